@@ -1,0 +1,372 @@
+/*
+ * tcm_oracle.c -- TEST INFRASTRUCTURE ONLY (see tcm_oracle.h).
+ *
+ * A plain, slow, obviously-correct CPU simulator of TCM-Serve's per-iteration
+ * scheduling step (arxiv 2603.26498).  It follows SURVEY.md 8(c) step by step:
+ * every decision re-keys EVERY pending request and fully sorts them (no class-FIFO
+ * merge, no fast-forward, no incremental state).  Build: gcc -O2 -ffp-contract=off,
+ * no fast-math (every floating-point operation is written out).
+ *
+ * Parity pins: tests/test_oracle_*.py (-m "not gpu").  Parity status per function is
+ * listed in DESIGN.md "Oracle pins".
+ */
+#include "tcm_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------ */
+/* K1 constants, transcribed from DESIGN.md "K1 constants" (hex floats).           */
+/* ------------------------------------------------------------------------------ */
+static const double ORC_LN2 = 0x1.62e42fefa39efp-1;
+
+/* LN reduction table: R[j] = k_j / 256, LT[j] = -ln(R[j]) rounded to nearest. */
+static const double ORC_LN_R[16] = {
+    0x1.f000000000000p-1, 0x1.d400000000000p-1, 0x1.ba00000000000p-1, 0x1.a400000000000p-1,
+    0x1.9000000000000p-1, 0x1.7e00000000000p-1, 0x1.6c00000000000p-1, 0x1.5c00000000000p-1,
+    0x1.4e00000000000p-1, 0x1.4200000000000p-1, 0x1.3600000000000p-1, 0x1.2a00000000000p-1,
+    0x1.2000000000000p-1, 0x1.1600000000000p-1, 0x1.0c00000000000p-1, 0x1.0400000000000p-1};
+static const double ORC_LN_LT[16] = {
+    0x1.0415d89e74444p-5, 0x1.700d30aeac0e1p-4, 0x1.2d1610c86813ap-3, 0x1.95a5adcf7017fp-3,
+    0x1.f991c6cb3b379p-3, 0x1.2bef07cdc9354p-2, 0x1.5d5bddf595f30p-2, 0x1.8b639a88b2df5p-2,
+    0x1.b56fa04462909p-2, 0x1.dae75484c9616p-2, 0x1.00e5ae5b207abp-1, 0x1.151c3f6f29612p-1,
+    0x1.269621134db92p-1, 0x1.38ae2171976e7p-1, 0x1.4b6fd6f970c1fp-1, 0x1.5af405c3649e0p-1};
+/* ln(1+u) series coefficients c_n = (-1)^(n+1)/n, n = 1..9 (index n-1). */
+static const double ORC_LN_C[9] = {
+    0x1.0000000000000p+0, -0x1.0000000000000p-1, 0x1.5555555555555p-2, -0x1.0000000000000p-2,
+    0x1.999999999999ap-3, -0x1.5555555555555p-3, 0x1.2492492492492p-3, -0x1.0000000000000p-3,
+    0x1.c71c71c71c71cp-4};
+
+static const double ORC_INV_LN2_16 = 0x1.71547652b82fep+4;
+static const double ORC_LN2_16_HI = 0x1.62e42fee00000p-5;
+static const double ORC_LN2_16_LO = 0x1.a39ef35793c76p-37;
+static const double ORC_EXP_T[16] = {
+    0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0, 0x1.2387a6e756238p+0,
+    0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,
+    0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0, 0x1.ea4afa2a490dap+0};
+/* 1/n!, n = 0..6 */
+static const double ORC_EXP_E[7] = {
+    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
+    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10};
+
+static uint64_t orc_bits(double d) { uint64_t b; memcpy(&b, &d, 8); return b; }
+static double orc_from_bits(uint64_t b) { double d; memcpy(&d, &b, 8); return d; }
+
+/* LN(v): DESIGN.md "K1" step LN.1-LN.6.  v must be a positive normal double. */
+double orc_ln(double v)
+{
+    uint64_t bits = orc_bits(v);
+    int e = (int)((bits >> 52) & 0x7FF) - 1023;                 /* LN.1 exponent   */
+    int j = (int)((bits >> 48) & 0xF);                          /* LN.2 table index */
+    double m = orc_from_bits((bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull);
+    double u = fma(m, ORC_LN_R[j], -1.0);                       /* LN.3            */
+    double q = ORC_LN_C[8];                                      /* LN.4 Horner     */
+    for (int i = 7; i >= 0; --i) q = fma(q, u, ORC_LN_C[i]);
+    double lnm = q * u;                                          /* LN.5            */
+    double t = ORC_LN_LT[j] + lnm;
+    return fma((double)e, ORC_LN2, t);                           /* LN.6            */
+}
+
+/* EXP(y): DESIGN.md "K1" step EXP.1-EXP.7. */
+double orc_exp(double y)
+{
+    if (y < -745.0) return 0.0;                                  /* EXP.1 */
+    if (y > 700.0) return INFINITY;
+    double kf = rint(y * ORC_INV_LN2_16);                        /* EXP.2 half-even */
+    double r = fma(-kf, ORC_LN2_16_HI, y);                       /* EXP.3 */
+    r = fma(-kf, ORC_LN2_16_LO, r);
+    double p = ORC_EXP_E[6];                                     /* EXP.4 Horner */
+    for (int i = 5; i >= 0; --i) p = fma(p, r, ORC_EXP_E[i]);
+    int64_t k = (int64_t)kf;                                     /* EXP.5 */
+    int64_t j = k & 15;
+    int64_t n = (k - j) / 16;
+    double s = ORC_EXP_T[j] * p;                                 /* EXP.6 */
+    if (n < -1021) return 0.0;                                   /* EXP.7 flush */
+    double res = s * orc_from_bits((uint64_t)(n + 1023) << 52);
+    if (res < 0x1p-1022) return 0.0;
+    return res;
+}
+
+/* C_c = LN(alpha*k_c) - p_c * LN(10^6): converts w in microseconds to seconds (R1). */
+double orc_k1_const(double alpha, double k, double p, int* zero_rate)
+{
+    double a = alpha * k;
+    if (!(a >= 0x1p-1022)) { *zero_rate = 1; return 0.0; }
+    *zero_rate = 0;
+    double t = p * orc_ln(1000000.0);
+    return orc_ln(a) - t;
+}
+
+/* Priority_c = StaticPriority_c + (1 - e^{-k_c * waiting_time^{p_c}}). */
+double orc_priority(double S, double p, double C, int zero_rate, uint64_t w_us)
+{
+    if (w_us == 0 || zero_rate) return S;
+    double v = (double)w_us;
+    double L = orc_ln(v);
+    double y = fma(p, L, C);
+    double x = orc_exp(y);
+    double e = orc_exp(-x);
+    return S + (1.0 - e);
+}
+
+/* Score = -log(Priority) is strictly decreasing, so ordering by max(P, eps)
+ * descending is the same order (R3). */
+uint64_t orc_key_bits(double priority)
+{
+    double q = priority < 1e-12 ? 1e-12 : priority;
+    return orc_bits(q);
+}
+
+/* Smart classifier represented by per-modality footprint thresholds (R13). */
+int orc_classify(const orc_model* m, uint8_t modality, uint32_t footprint)
+{
+    if (footprint < m->thr_mc[modality]) return 0;   /* motorcycle */
+    if (footprint < m->thr_ct[modality]) return 1;   /* car        */
+    return 2;                                         /* truck      */
+}
+
+/* Isolated (no-contention) TTFT / E2E, SPEC.md:141-149 in integer microseconds (R9). */
+uint64_t orc_iso_ttft(const orc_model* m, uint32_t B, uint32_t f, uint32_t inl)
+{
+    uint64_t chunks = ((uint64_t)f + B - 1) / B;
+    return (uint64_t)inl + chunks * m->c0_us + m->cp_us * (uint64_t)f;
+}
+
+uint64_t orc_iso_e2e(const orc_model* m, uint32_t B, uint32_t f, uint32_t inl, uint16_t out)
+{
+    return orc_iso_ttft(m, B, f, inl) + (uint64_t)(out - 1) * (m->c0_us + m->cd_us);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* The engine loop: SURVEY.md 8(c) steps 1-10.    */
+/* ------------------------------------------------------------------------------ */
+typedef struct {
+    double   P;
+    uint64_t arrival;
+    uint32_t id;
+} orc_entry;
+
+/* Order: priority descending, then arrival ascending, then id ascending (R4). */
+static int orc_cmp(const void* a, const void* b)
+{
+    const orc_entry* x = (const orc_entry*)a;
+    const orc_entry* y = (const orc_entry*)b;
+    uint64_t kx = orc_key_bits(x->P), ky = orc_key_bits(y->P);
+    if (kx != ky) return kx > ky ? -1 : 1;
+    if (x->arrival != y->arrival) return x->arrival < y->arrival ? -1 : 1;
+    if (x->id != y->id) return x->id < y->id ? -1 : 1;
+    return 0;
+}
+
+int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
+                 const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
+                 const uint16_t* out, const uint8_t* mod, uint32_t* admit_seq,
+                 uint64_t* first_token, uint64_t* done, uint8_t* cls_out,
+                 orc_counters* cnt, orc_iter_rec* log, uint64_t log_cap, uint64_t* log_n)
+{
+    memset(cnt, 0, sizeof(*cnt));
+    if (log_n) *log_n = 0;
+    if (r->chunk_budget == 0 || r->policy > ORC_TCM) return -1;
+    for (uint32_t i = 0; i < n; ++i) {
+        if (f[i] == 0 || f[i] > r->kv_capacity || out[i] == 0 || mod[i] > 2) return -1;
+        if (i > 0 && arrival[i] < arrival[i - 1]) return -1;
+    }
+
+    double C[3];
+    int zero[3];
+    for (int c = 0; c < 3; ++c) C[c] = orc_k1_const(r->alpha, m->k[c], m->p[c], &zero[c]);
+
+    uint32_t* pending = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1));
+    uint32_t* decoding = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1));
+    uint32_t* rem = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1));
+    uint32_t* gen = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1));
+    uint8_t* reserved = (uint8_t*)calloc(n + 1, 1);
+    orc_entry* order = (orc_entry*)malloc(sizeof(orc_entry) * (n + 1));
+    if (!pending || !decoding || !rem || !gen || !reserved || !order) {
+        free(pending); free(decoding); free(rem); free(gen); free(reserved); free(order);
+        return -1;
+    }
+
+    uint64_t clock = 0, kv_free = r->kv_capacity, iter = 0;
+    uint32_t nxt = 0, seq = 0, n_pend = 0, n_dec = 0;
+    int status = 0;
+
+    for (;;) {
+        /* 1 ingest arrivals <= clock, classify on ingest */
+        while (nxt < n && arrival[nxt] <= clock) {
+            cls_out[nxt] = (uint8_t)orc_classify(m, mod[nxt], f[nxt]);
+            rem[nxt] = f[nxt];
+            reserved[nxt] = 0;
+            pending[n_pend++] = nxt;
+            ++nxt;
+        }
+        /* 2 idle: jump to the next arrival (R15), not an iteration */
+        if (n_pend == 0 && n_dec == 0) {
+            if (nxt == n) break;
+            clock = arrival[nxt];
+            cnt->idle_jumps++;
+            continue;
+        }
+        orc_iter_rec rec;
+        memset(&rec, 0, sizeof(rec));
+        rec.clock_start = clock;
+        rec.kv_free_start = kv_free;
+        rec.n_pending = n_pend;
+        rec.n_dec = n_dec;
+
+        /* 3 budget left after decodes (R8) */
+        uint32_t Bp = r->chunk_budget > n_dec ? r->chunk_budget - n_dec : 0;
+        rec.budget = Bp;
+
+        /* 4-5 key every pending request and sort (TCM), or arrival order (FCFS) */
+        for (uint32_t q = 0; q < n_pend; ++q) {
+            uint32_t i = pending[q];
+            order[q].id = i;
+            order[q].arrival = arrival[i];
+            if (r->policy == ORC_TCM) {
+                int c = cls_out[i];
+                order[q].P = orc_priority(m->S[c], m->p[c], C[c], zero[c], clock - arrival[i]);
+            } else {
+                order[q].P = 0.0;
+            }
+        }
+        if (r->policy == ORC_TCM) qsort(order, n_pend, sizeof(orc_entry), orc_cmp);
+
+        /* 6 admission scan: greedy chunks; first KV misfit blocks later NEW admits (R6) */
+        uint32_t left = Bp;
+        int blocked = 0;
+        uint64_t tok = 0, inl_sum = 0;
+        for (uint32_t q = 0; q < n_pend; ++q) {
+            uint32_t i = order[q].id;
+            if (left == 0) break;
+            if (!reserved[i]) {
+                if (blocked) continue;
+                if ((uint64_t)f[i] > kv_free) { blocked = 1; continue; }
+                reserved[i] = 1;
+                kv_free -= f[i];
+                admit_seq[i] = seq++;
+                inl_sum += inl[i];
+                rec.n_admitted++;
+            }
+            uint32_t c = rem[i] < left ? rem[i] : left;
+            rem[i] -= c;
+            left -= c;
+            tok += c;
+        }
+        rec.kv_free_admit = kv_free;
+        rec.tokens = (uint32_t)tok;
+
+        /* 7 progress is guaranteed under R6 */
+        if (tok == 0 && n_dec == 0) { status = -2; break; }
+
+        /* 8 iteration cost and clock (R9, R10) */
+        clock += m->c0_us + m->cp_us * tok + m->cd_us * (uint64_t)n_dec + inl_sum;
+        iter++;
+        cnt->iterations++;
+        if (n_pend > 0) {                     /* R17: only iterations with pending work */
+            cnt->decisions++;
+            cnt->sum_pending += n_pend;
+            if (n_pend > cnt->max_pending) cnt->max_pending = n_pend;
+        }
+
+        /* 9 every decoding sequence emits one token; finished ones release KV (R7) */
+        uint32_t kept = 0;
+        for (uint32_t q = 0; q < n_dec; ++q) {
+            uint32_t d = decoding[q];
+            gen[d]++;
+            if (gen[d] == out[d]) {
+                done[d] = clock;
+                kv_free += f[d];
+            } else {
+                decoding[kept++] = d;
+            }
+        }
+        n_dec = kept;
+
+        /* 10 requests whose prefill completed emit their first token now (R12) */
+        kept = 0;
+        for (uint32_t q = 0; q < n_pend; ++q) {
+            uint32_t i = pending[q];
+            if (reserved[i] && rem[i] == 0) {
+                first_token[i] = clock;
+                gen[i] = 1;
+                rec.n_first_tokens++;
+                if (out[i] == 1) {
+                    done[i] = clock;
+                    kv_free += f[i];
+                } else {
+                    decoding[n_dec++] = i;
+                }
+            } else {
+                if (reserved[i]) rec.n_partial_after++;
+                pending[kept++] = i;
+            }
+        }
+        n_pend = kept;
+        rec.clock_end = clock;
+        if (log && *log_n < log_cap) log[*log_n] = rec;
+        if (log_n) (*log_n)++;
+    }
+    cnt->admitted = seq;
+    cnt->final_clock = clock;
+
+    free(pending); free(decoding); free(rem); free(gen); free(reserved); free(order);
+    return status;
+}
+
+/* ------------------------------------------------------------------------------ */
+/* a6: result aggregation (PAPER.md:579 SLO = 5x isolated E2E).   */
+/* ------------------------------------------------------------------------------ */
+
+/* HDR-style log bucket: t < 16 -> t; else with
+ * e = floor(log2 t): 16 + 8*(e-4) + the 3 bits below the leading one. */
+uint32_t orc_ttft_bucket(uint64_t t)
+{
+    if (t < 16) return (uint32_t)t;
+    uint32_t e = 0;
+    while (e < 63 && (t >> (e + 1)) != 0) ++e;   /* e = floor(log2 t), plain loop */
+    return 16u + 8u * (e - 4u) + (uint32_t)((t >> (e - 3u)) & 7u);
+}
+
+void orc_aggregate(const orc_model* m, uint32_t B, uint32_t n, const uint64_t* arrival,
+                   const uint32_t* f, const uint32_t* inl, const uint16_t* out,
+                   const uint8_t* mod, const uint64_t* first_token, const uint64_t* done,
+                   int64_t* hist, int64_t* cnt)
+{
+    for (uint32_t i = 0; i < n; ++i) {
+        int g = orc_classify(m, mod[i], f[i]);
+        uint64_t ttft = first_token[i] - arrival[i];
+        uint64_t e2e = done[i] - arrival[i];
+        uint64_t iso = orc_iso_e2e(m, B, f[i], inl[i], out[i]);
+        uint64_t lhs = e2e * m->slo_den, rhs = iso * m->slo_num;
+        int viol = lhs > rhs;
+        int groups[2] = {g, 3};
+        for (int k = 0; k < 2; ++k) {
+            int gg = groups[k];
+            hist[gg * ORC_HIST_BINS + orc_ttft_bucket(ttft)] += 1;
+            int64_t* c = cnt + gg * ORC_NCNT;
+            c[0] += 1;                                  /* n                         */
+            c[1] += (int64_t)ttft;                      /* sum TTFT (us)             */
+            c[2] += (int64_t)e2e;                       /* sum E2E (us)              */
+            c[3] += viol;                               /* SLO violations            */
+            c[4] += viol ? (int64_t)(lhs - rhs) : 0;    /* sum severity x den (us)   */
+            c[5] += (int64_t)(e2e / out[i]);            /* sum normalized lat (us/tok)*/
+        }
+    }
+}
+
+/* Lemma L1 audit: first w in [w_lo, w_hi) with key(w+1) < key(w),
+ * or UINT64_MAX if K1 is non-decreasing on the whole range. Plain loop. */
+uint64_t orc_audit_monotone(double S, double p, double C, int zero_rate,
+                            uint64_t w_lo, uint64_t w_hi)
+{
+    uint64_t prev = orc_key_bits(orc_priority(S, p, C, zero_rate, w_lo));
+    for (uint64_t w = w_lo + 1; w <= w_hi; ++w) {
+        uint64_t k = orc_key_bits(orc_priority(S, p, C, zero_rate, w));
+        if (k < prev) return w - 1;
+        prev = k;
+    }
+    return UINT64_MAX;
+}

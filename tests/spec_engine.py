@@ -1,0 +1,96 @@
+"""A second, declarative statement of the scheduling step, used ONLY to pin the oracle.
+
+Written from PAPER.md:315, 447-461, 572, 580 and SPEC.md:131-144, 394-403, 455 with the
+readings R1-R25, in a deliberately different shape from oracle/tcm_oracle.c:
+per-request dicts, Python's sorted() with a tuple key, and the paper's priority formula
+evaluated with Python's math library (not K1).  Because math.exp/pow differ from K1 in the
+last bits, callers must discard traces whose order depends on a near-tie
+(`near_tie` is set when two keys of different classes are within 1e-11 of each other).
+"""
+from __future__ import annotations
+
+import math
+
+S = (0.1, 0.05, 0.0)
+K = (0.05, 0.003, 0.00075)
+P = (3.5, 2.5, 1.1)
+
+
+def paper_priority(c, w_us, alpha):
+    if w_us == 0 or alpha == 0.0:
+        return S[c]
+    return S[c] + (1.0 - math.exp(-alpha * K[c] * (w_us / 1e6) ** P[c]))
+
+
+def classify(mod, f, thr):
+    mc, ct = thr[mod]
+    return 0 if f < mc else (1 if f < ct else 2)
+
+
+def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
+        thr=((4096, 2**32 - 1), (0, 2**32 - 1), (0, 8192))):
+    """reqs: list of (arrival_us, footprint, inline_us, out, modality). Returns dict of lists."""
+    n = len(reqs)
+    R = [dict(id=i, arr=a, f=f, inl=il, out=o, cls=classify(m, f, thr), state="future",
+              rem=f, gen=0, admit=None, first=None, done=None)
+         for i, (a, f, il, o, m) in enumerate(reqs)]
+    clock, free, seq = 0, kv, 0
+    near_tie = False
+    while True:
+        for r in R:                                       # step 1: ingest
+            if r["state"] == "future" and r["arr"] <= clock:
+                r["state"] = "waiting"
+        pend = [r for r in R if r["state"] in ("waiting", "partial")]
+        dec = [r for r in R if r["state"] == "decoding"]
+        if not pend and not dec:                          # step 2: idle jump
+            fut = [r["arr"] for r in R if r["state"] == "future"]
+            if not fut:
+                break
+            clock = min(fut)
+            continue
+        budget = max(0, B - len(dec))                     # step 3 (R8)
+        if policy == 1:                                   # steps 4-5 (R2-R5)
+            keyed = [(max(paper_priority(r["cls"], clock - r["arr"], alpha), 1e-12), r) for r in pend]
+            vals = sorted(keyed, key=lambda t: -t[0])
+            for (pa, ra), (pb, rb) in zip(vals, vals[1:]):
+                if ra["cls"] != rb["cls"] and abs(pa - pb) < 1e-11:
+                    near_tie = True
+            order = [r for _, r in sorted(keyed, key=lambda t: (-t[0], t[1]["arr"], t[1]["id"]))]
+        else:
+            order = sorted(pend, key=lambda r: (r["arr"], r["id"]))
+        left, blocked, tok, inl = budget, False, 0, 0     # step 6 (R6, R7)
+        for r in order:
+            if left == 0:
+                break
+            if r["state"] == "waiting":
+                if blocked:
+                    continue
+                if r["f"] > free:
+                    blocked = True
+                    continue
+                r["state"] = "partial"
+                free -= r["f"]
+                r["admit"] = seq
+                seq += 1
+                inl += r["inl"]
+            chunk = min(r["rem"], left)
+            r["rem"] -= chunk
+            left -= chunk
+            tok += chunk
+        assert tok > 0 or dec, "deadlock"
+        clock += c0 + cp * tok + cd * len(dec) + inl      # step 8
+        for r in dec:                                     # step 9
+            r["gen"] += 1
+            if r["gen"] == r["out"]:
+                r["state"], r["done"] = "finished", clock
+                free += r["f"]
+        for r in pend:                                    # step 10 (R12)
+            if r["state"] == "partial" and r["rem"] == 0:
+                r["first"], r["gen"] = clock, 1
+                if r["out"] == 1:
+                    r["state"], r["done"] = "finished", clock
+                    free += r["f"]
+                else:
+                    r["state"] = "decoding"
+    return dict(admit_seq=[r["admit"] for r in R], first=[r["first"] for r in R],
+                done=[r["done"] for r in R], near_tie=near_tie)
