@@ -1,0 +1,213 @@
+/*
+ * tcm.h -- C ABI of libtcm: TCM-Serve's per-iteration modality-aware scheduling step
+ * (arxiv 2603.26498, Section 3) run as a trace-driven simulation over many
+ * independent replicas on one B200 (sm_100a).
+ *
+ * Every replica is one serving engine (vLLM V1 + chunked prefill) fed by
+ * its own request trace.  Each engine iteration, per replica:
+ *   a1 ingest arrivals <= clock and classify them motorcycle / car / truck from modality
+ *      and KV footprint (reading R13);
+ *   a2 key every pending request with Priority_c = S_c + (1 - e^{-k_c w^{p_c}})
+ *      (PAPER.md:457, 580), evaluated by the specified-arithmetic K1;
+ *   a3 order pending requests by key (Score = -log Priority; R3, R4);
+ *   a4 admit a prefill batch by prefix-scanning chunk tokens against the chunked-prefill
+ *      budget and footprints against free KV (R5-R8);
+ *   a5 advance an integer-microsecond clock by c0 + cp*tokens + cd*decodes + inline
+ *      (R9, R10) and record TTFT / completion (R12);
+ *   a6 aggregate TTFT histograms and SLO counters.
+ *
+ * Conventions for every entry point:
+ *   - No exception crosses the ABI; every call returns a tcm_status (0 = OK, < 0 error)
+ *     and records a message retrievable with tcm_last_error().
+ *   - Buffers are caller-owned.  "device" pointers are CUDA device memory on the
+ *     context's device; "host" pointers are ordinary or pinned host memory (pinned is
+ *     required for asynchronous overlap but not for correctness).  The library borrows
+ *     every pointer from tcm_load_trace until tcm_destroy / the next tcm_load_trace.
+ *   - All work is enqueued on the caller's CUDA stream given to tcm_create; tcm_run,
+ *     tcm_step and tcm_stats synchronise that stream before returning.
+ *   - Results are deterministic: independent of launch geometry, engine, stream and of
+ *     how replicas are split across GPUs (every reduction is an integer sum).
+ *   - A context is not thread-safe; distinct contexts are independent.
+ */
+#ifndef TCM_H
+#define TCM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCM_ABI_VERSION 1u
+
+typedef int32_t tcm_status;
+#define TCM_OK 0
+#define TCM_E_ARG (-1)      /* invalid argument or malformed trace                      */
+#define TCM_E_STATE (-2)    /* calls out of order (e.g. tcm_run before tcm_load_trace)   */
+#define TCM_E_CAPACITY (-3) /* a footprint exceeds its replica's KV capacity (SPEC.md:456
+                               CapacityImpossible; R18)                                 */
+#define TCM_E_CUDA (-4)     /* a CUDA runtime call failed                                */
+#define TCM_E_OOM (-5)      /* workspace allocation failed                               */
+#define TCM_E_REPLICA (-6)  /* >= 1 replica set a device status (deadlock assertion,
+                               unreachable under R6; see tcm_stats_host.first_bad_*)     */
+#define TCM_E_VERSION (-7)  /* abi_version mismatch                                      */
+
+enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1 };
+/* FCFS: vLLM's single arrival-ordered queue with chunked prefill.
+ * TCM : three class queues + aging priority.  Static priority
+ *        is TCM with aging_alpha = 0 (R14). */
+
+enum { TCM_ENGINE_FUSED = 0, TCM_ENGINE_STEPWISE = 1 };
+/* FUSED   : one persistent thread per replica runs the whole step loop in registers;
+ *           a3 is the exact 3-way merge of the class-FIFO heads (Lemma L1).
+ * STEPWISE: the paper-literal step -- per iteration, every pending request of every
+ *           active replica is re-keyed (a1+a2), top-k selected (a3), prefix-scanned (a4),
+ *           then the clock kernel runs (a5).  Bit-identical results; used for the
+ *           per-step HBM roofline and for key functions that are not class-monotone. */
+
+enum { TCM_MEM_DEVICE = 0, TCM_MEM_HOST = 1 };
+
+/* Model-wide constants (one per context).  All times are integer microseconds (R9). */
+typedef struct tcm_config {
+    uint32_t abi_version;  /* = TCM_ABI_VERSION                                     */
+    uint32_t engine;       /* TCM_ENGINE_*                                          */
+    uint64_t c0_us;        /* per-iteration overhead (5 ms)            */
+    uint64_t cp_us;        /* per prefill token (20 us)                */
+    uint64_t cd_us;        /* per decoding sequence (0.5 ms)           */
+    double S[3];           /* StaticPriority_c for M, C, T (.1,.05,0) */
+    double k[3];           /* k_c (0.05, 0.003, 0.00075)              */
+    double p[3];           /* p_c (3.5, 2.5, 1.1)                     */
+    uint32_t thr_mc[3];    /* per modality (text,image,video): footprint < thr_mc -> M */
+    uint32_t thr_ct[3];    /* per modality: footprint < thr_ct -> C, else T (R13)   */
+    uint32_t slo_num;      /* SLO = slo_num/slo_den x isolated E2E   */
+    uint32_t slo_den;
+    uint32_t n_cells;      /* sweep cells for the a6 aggregation (>= 1)             */
+    uint32_t reserved;     /* must be 0                                             */
+} tcm_config;
+
+/* Per-replica parameters (one sweep point x seed).  32 bytes. */
+typedef struct tcm_replica_params {
+    uint32_t policy;       /* TCM_POLICY_*                                          */
+    uint32_t chunk_budget; /* B: chunked-prefill tokens per iteration, >= 1 */
+    uint64_t kv_capacity;  /* KV tokens, 1 .. 2^32-1    */
+    double aging_alpha;    /* multiplies every k_c, >= 0 (R14)                      */
+    uint32_t cell_id;      /* < n_cells: aggregation cell                           */
+    uint32_t reserved;     /* must be 0                                             */
+} tcm_replica_params;
+
+/* The request trace, SoA in CSR form: replica r owns requests [req_offset[r], req_offset[r+1]),
+ * sorted by (arrival, id) -- ids are the local indices 0..n_r-1 (R4, R16). */
+typedef struct tcm_trace_view {
+    uint32_t mem;                 /* TCM_MEM_DEVICE or TCM_MEM_HOST (all arrays alike)  */
+    uint32_t n_replicas;          /* R >= 1                                             */
+    uint64_t n_requests;          /* = req_offset[R]; each replica has < 2^32 - 1        */
+    const uint64_t* req_offset;   /* [R+1], req_offset[0] = 0, non-decreasing           */
+    const uint64_t* arrival_us;   /* [N] non-decreasing within a replica                */
+    const uint32_t* footprint;    /* [N] prompt + media tokens = KV footprint, 1..kv_capacity */
+    const uint32_t* inline_us;    /* [N] preprocess + encode time, charged inline (R10) */
+    const uint16_t* out_tokens;   /* [N] output tokens, 1..2048 (R23)                   */
+    const uint8_t* modality;      /* [N] 0 text, 1 image, 2 video                       */
+    const tcm_replica_params* params; /* [R]                                            */
+} tcm_trace_view;
+
+/* Per-request outputs, written in place (any pointer may be NULL: then the library keeps
+ * the values in its workspace for tcm_stats only). */
+typedef struct tcm_results_view {
+    uint32_t mem;                 /* TCM_MEM_DEVICE or TCM_MEM_HOST                     */
+    uint32_t reserved;
+    uint32_t* admit_seq;          /* [N] order of first admission within the replica    */
+    uint64_t* first_token_us;     /* [N] clock at the first token (TTFT = - arrival)    */
+    uint64_t* done_us;            /* [N] clock at completion                            */
+} tcm_results_view;
+
+/* Work counters (sums over all replicas of this context). */
+typedef struct tcm_stats_host {
+    uint64_t iterations;       /* engine iterations, fast-forwarded ones included    */
+    uint64_t decisions;        /* iterations with >= 1 pending request (R17)         */
+    uint64_t ff_iterations;    /* iterations covered by decode-only fast-forward     */
+    uint64_t idle_jumps;       /* jumps of an empty engine to its next arrival (R15) */
+    uint64_t sum_pending;      /* sum over decisions of the pending-set size         */
+    uint64_t max_pending;      /* max over decisions and replicas                    */
+    uint64_t requests_done;    /* requests with done_us stamped                      */
+    uint64_t replicas_done;
+    uint64_t replicas_active;
+    uint64_t kernel_launches;  /* library kernels launched since tcm_create          */
+    int32_t first_bad_replica; /* -1 if none                                          */
+    int32_t first_bad_status;
+} tcm_stats_host;
+
+typedef struct tcm_ctx tcm_ctx;
+
+/* Synthetic-trace generator descriptor (layout of tracegen/tcm_tracegen.h tg_replica). */
+typedef struct tcm_gen_replica {
+    uint64_t seed;          /* splitmix64(base ^ replica)                            */
+    uint64_t kv_capacity;   /* footprints are clamped to this (R18)                  */
+    double mean_gap_us;     /* 1e6 / lambda: Poisson arrivals         */
+    uint64_t mix_t1;        /* 32-bit draw < mix_t1 -> text                          */
+    uint64_t mix_t2;        /* draw < mix_t2 -> image, else video     */
+    uint32_t n_requests;
+    uint32_t flags;         /* bit0: every arrival at t = 0                          */
+} tcm_gen_replica;
+
+/* Validates *cfg and creates a context bound to the current CUDA device and `cuda_stream`
+ * (a cudaStream_t; NULL = legacy default stream).  Errors: TCM_E_ARG, TCM_E_VERSION. */
+tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out);
+
+/* Binds a trace and result buffers, allocates the workspace (tcm_workspace_bytes) and
+ * validates the trace on the device: footprint <= kv_capacity (TCM_E_CAPACITY), and
+ * footprint >= 1, 1 <= out <= 2048, modality <= 2, non-decreasing arrivals, params in
+ * range (TCM_E_ARG).  HOST traces are copied to the device here (on the stream).
+ * Resets every replica to its initial state (clock 0, all KV free). */
+tcm_status tcm_load_trace(tcm_ctx* ctx, const tcm_trace_view* trace,
+                          const tcm_results_view* results);
+
+/* Advances every unfinished replica by at most max_iterations engine iterations (a
+ * fast-forward counts all the iterations it covers; idle jumps count none).  Writes the
+ * number of replicas still unfinished to *active_replicas (may be NULL).  HOST results
+ * are copied back before returning. */
+tcm_status tcm_step(tcm_ctx* ctx, uint32_t max_iterations, uint32_t* active_replicas);
+
+/* Runs every replica to completion (every request done).  TCM_E_REPLICA if a replica
+ * hit its deadlock assertion. */
+tcm_status tcm_run(tcm_ctx* ctx);
+
+/* Fills *out (may be NULL) and, when dev_hist / dev_cnt are non-NULL, writes the a6
+ * aggregation: dev_hist[n_cells][4][496] and dev_cnt[n_cells][4][6] (int64, DEVICE,
+ * overwritten; groups M, C, T, all; counters n, sum TTFT, sum E2E, SLO violations,
+ * sum (e2e*den - num*iso) over violators, sum floor(e2e/out)).  These buffers are
+ * NCCL-ready: all-reduce(SUM) across GPUs gives the bit-exact global result. */
+tcm_status tcm_stats(tcm_ctx* ctx, tcm_stats_host* out, int64_t* dev_hist, int64_t* dev_cnt);
+
+/* Releases the workspace and the context (NULL is a no-op). */
+void tcm_destroy(tcm_ctx* ctx);
+
+/* Message of the last failing call on ctx ("" if none; ctx NULL -> last global error). */
+const char* tcm_last_error(const tcm_ctx* ctx);
+
+/* Device bytes the library allocates for a trace of this shape (excluding caller buffers,
+ * including mirrors of HOST traces / results when `host_mirror` is non-zero). */
+size_t tcm_workspace_bytes(const tcm_config* cfg, uint32_t n_replicas, uint64_t n_requests,
+                           int host_mirror);
+
+/* Generates traces on the device (bit-identical to tracegen/ on the host): replica r
+ * fills [req_offset[r], req_offset[r+1]), which must equal reps[r].n_requests.  All
+ * pointers are DEVICE.  Enqueued on cuda_stream; synchronises it. */
+tcm_status tcm_generate_trace(const tcm_gen_replica* reps, uint32_t n_replicas,
+                              const uint64_t* req_offset, uint64_t* arrival_us,
+                              uint32_t* footprint, uint32_t* inline_us, uint16_t* out_tokens,
+                              uint8_t* modality, void* cuda_stream);
+
+/* Diagnostics for the K1 key, DEVICE pointers:
+ * tcm_k1_eval writes P = K1(cls[i], w[i]) for alpha[i] (n elements) using cfg's S,k,p;
+ * tcm_k1_audit writes to *first_violation (device u64) the smallest w in [w_lo, w_hi)
+ * with key(w+1) < key(w) for class `cls` and `alpha` (UINT64_MAX if none). */
+tcm_status tcm_k1_eval(const tcm_config* cfg, const uint8_t* cls, const uint64_t* w,
+                       const double* alpha, double* out_priority, uint64_t n, void* cuda_stream);
+tcm_status tcm_k1_audit(const tcm_config* cfg, uint32_t cls, double alpha, uint64_t w_lo,
+                        uint64_t w_hi, uint64_t* first_violation, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

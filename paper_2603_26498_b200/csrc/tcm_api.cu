@@ -1,0 +1,436 @@
+// tcm_api.cu -- the C ABI of libtcm (include/tcm.h): context, trace binding, workspace,
+// engine dispatch, statistics.  Host-side orchestration only; every step of the
+// scheduling path runs in the kernels of tcm_fused.cu / tcm_stepwise.cu / tcm_aux.cu.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tcm_aux.cuh"
+#include "tcm_internal.cuh"
+#include "tcm_stepwise.cuh"
+
+using namespace tcm;
+
+struct tcm_ctx {
+    tcm_config cfg{};
+    ModelConst m{};
+    cudaStream_t s = nullptr;
+    int device = 0;
+    std::string err;
+    bool loaded = false;
+    TraceDev t{};
+    std::vector<void*> allocs;           // workspace + HOST mirrors, freed on reload/destroy
+    bool host_results = false;
+    tcm_results_view host_res{};
+    uint32_t* d_active = nullptr;        // [1]
+    unsigned long long* d_acc = nullptr; // [kAccN]
+    uint32_t* d_val = nullptr;           // [2]
+    StepwiseWorkspace sw{};
+    uint64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+tcm_status fail(tcm_ctx* c, tcm_status code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    g_err = buf;
+    return code;
+}
+
+#define TCM_CUDA(ctx, call)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail((ctx), TCM_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));    \
+    } while (0)
+
+void free_allocs(tcm_ctx* c) {
+    for (void* p : c->allocs) cudaFree(p);
+    c->allocs.clear();
+    c->loaded = false;
+    c->sw = StepwiseWorkspace{};
+}
+
+tcm_status dalloc(tcm_ctx* c, void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TCM_E_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+    c->allocs.push_back(*p);
+    return TCM_OK;
+}
+
+tcm_status validate_config(const tcm_config* cfg) {
+    if (!cfg) return fail(nullptr, TCM_E_ARG, "config is NULL");
+    if (cfg->abi_version != TCM_ABI_VERSION)
+        return fail(nullptr, TCM_E_VERSION, "abi_version %u != %u", cfg->abi_version, TCM_ABI_VERSION);
+    if (cfg->engine > TCM_ENGINE_STEPWISE) return fail(nullptr, TCM_E_ARG, "bad engine %u", cfg->engine);
+    if (cfg->slo_den == 0 || cfg->n_cells == 0 || cfg->reserved != 0)
+        return fail(nullptr, TCM_E_ARG, "slo_den and n_cells must be >= 1, reserved 0");
+    for (int c = 0; c < 3; ++c) {
+        if (!(cfg->k[c] >= 0.0) || !(cfg->p[c] > 0.0) || !(cfg->S[c] >= 0.0))
+            return fail(nullptr, TCM_E_ARG, "priority constants must be finite, k,S >= 0, p > 0");
+    }
+    return TCM_OK;
+}
+
+ModelConst to_model(const tcm_config& c) {
+    ModelConst m{};
+    m.c0 = c.c0_us;
+    m.cp = c.cp_us;
+    m.cd = c.cd_us;
+    for (int i = 0; i < 3; ++i) {
+        m.S[i] = c.S[i];
+        m.k[i] = c.k[i];
+        m.p[i] = c.p[i];
+        m.thr_mc[i] = c.thr_mc[i];
+        m.thr_ct[i] = c.thr_ct[i];
+    }
+    m.slo_num = c.slo_num;
+    m.slo_den = c.slo_den;
+    m.n_cells = c.n_cells;
+    return m;
+}
+
+size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) {
+    size_t b = 0;
+    b += 4 * N;                                  // link
+    b += (size_t)R * kCalSlots * 4;              // calendar heads
+    b += (size_t)R * kCalWords * 4;              // occupancy
+    b += (size_t)R * sizeof(ReplicaState);
+    b += 20 * N;                                 // results kept on device when not supplied
+    if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N);
+    if (host_mirror) b += (size_t)(R + 1) * 8 + 19 * N + (size_t)R * sizeof(tcm_replica_params);
+    return b;
+}
+
+tcm_status copy_results_to_host(tcm_ctx* c) {
+    if (!c->host_results) return TCM_OK;
+    const uint64_t N = c->t.N;
+    if (c->host_res.admit_seq)
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.admit_seq, c->t.admit_seq, 4 * N, cudaMemcpyDeviceToHost, c->s));
+    if (c->host_res.first_token_us)
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.first_token_us, c->t.first_token, 8 * N, cudaMemcpyDeviceToHost, c->s));
+    if (c->host_res.done_us)
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.done_us, c->t.done, 8 * N, cudaMemcpyDeviceToHost, c->s));
+    return TCM_OK;
+}
+
+tcm_status reduce_stats(tcm_ctx* c, unsigned long long* h) {
+    TCM_CUDA(c, cudaMemsetAsync(c->d_acc, 0, kAccN * 8, c->s));
+    TCM_CUDA(c, cudaMemsetAsync(c->d_acc + kAccBadReplica, 0xFF, 8, c->s));
+    launch_reduce(c->t, c->d_acc, c->s);
+    c->launches++;
+    TCM_CUDA(c, cudaGetLastError());
+    TCM_CUDA(c, cudaMemcpyAsync(h, c->d_acc, kAccN * 8, cudaMemcpyDeviceToHost, c->s));
+    TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    return TCM_OK;
+}
+
+tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
+    TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
+    if (c->cfg.engine == TCM_ENGINE_FUSED) {
+        launch_fused(c->m, c->t, max_iters, c->d_active, c->s);
+        c->launches++;
+    } else {
+        uint64_t l = 0;
+        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, &l);
+        c->launches += l;
+        if (st != TCM_OK) return fail(c, st, "stepwise engine failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    TCM_CUDA(c, cudaGetLastError());
+    TCM_CUDA(c, cudaMemcpyAsync(active, c->d_active, 4, cudaMemcpyDeviceToHost, c->s));
+    TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    return TCM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
+    if (!out) return fail(nullptr, TCM_E_ARG, "out is NULL");
+    *out = nullptr;
+    tcm_status st = validate_config(cfg);
+    if (st != TCM_OK) return st;
+    tcm_ctx* c = new (std::nothrow) tcm_ctx();
+    if (!c) return fail(nullptr, TCM_E_OOM, "context allocation failed");
+    c->cfg = *cfg;
+    c->m = to_model(*cfg);
+    c->s = reinterpret_cast<cudaStream_t>(cuda_stream);
+    cudaError_t e = cudaGetDevice(&c->device);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_active, 4);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_acc, kAccN * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 8);
+    if (e != cudaSuccess) {
+        fail(nullptr, TCM_E_CUDA, "tcm_create: %s", cudaGetErrorString(e));
+        cudaFree(c->d_active);
+        cudaFree(c->d_acc);
+        cudaFree(c->d_val);
+        delete c;
+        return TCM_E_CUDA;
+    }
+    *out = c;
+    return TCM_OK;
+}
+
+tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_results_view* rv) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!tv) return fail(c, TCM_E_ARG, "trace is NULL");
+    if (tv->n_replicas == 0) return fail(c, TCM_E_ARG, "n_replicas must be >= 1");
+    if (!tv->req_offset || !tv->params || (tv->n_requests > 0 && (!tv->arrival_us || !tv->footprint ||
+        !tv->inline_us || !tv->out_tokens || !tv->modality)))
+        return fail(c, TCM_E_ARG, "trace arrays must be non-NULL");
+    if (tv->mem > TCM_MEM_HOST || (rv && rv->mem > TCM_MEM_HOST)) return fail(c, TCM_E_ARG, "bad mem kind");
+    free_allocs(c);
+    const uint32_t R = tv->n_replicas;
+    const uint64_t N = tv->n_requests;
+    TraceDev t{};
+    t.R = R;
+    t.N = N;
+    cudaStream_t s = c->s;
+    tcm_status st;
+
+    if (tv->mem == TCM_MEM_HOST) {
+        if (tv->req_offset[R] != N || tv->req_offset[0] != 0)
+            return fail(c, TCM_E_ARG, "req_offset[R] (%llu) != n_requests (%llu)",
+                        (unsigned long long)tv->req_offset[R], (unsigned long long)N);
+        void *o, *a, *f, *il, *ou, *md, *pp;
+        if ((st = dalloc(c, &o, (R + 1) * 8ull)) || (st = dalloc(c, &a, 8 * N)) || (st = dalloc(c, &f, 4 * N)) ||
+            (st = dalloc(c, &il, 4 * N)) || (st = dalloc(c, &ou, 2 * N)) || (st = dalloc(c, &md, N)) ||
+            (st = dalloc(c, &pp, R * sizeof(tcm_replica_params))))
+            return st;
+        TCM_CUDA(c, cudaMemcpyAsync(o, tv->req_offset, (R + 1) * 8ull, cudaMemcpyHostToDevice, s));
+        TCM_CUDA(c, cudaMemcpyAsync(a, tv->arrival_us, 8 * N, cudaMemcpyHostToDevice, s));
+        TCM_CUDA(c, cudaMemcpyAsync(f, tv->footprint, 4 * N, cudaMemcpyHostToDevice, s));
+        TCM_CUDA(c, cudaMemcpyAsync(il, tv->inline_us, 4 * N, cudaMemcpyHostToDevice, s));
+        TCM_CUDA(c, cudaMemcpyAsync(ou, tv->out_tokens, 2 * N, cudaMemcpyHostToDevice, s));
+        TCM_CUDA(c, cudaMemcpyAsync(md, tv->modality, N, cudaMemcpyHostToDevice, s));
+        TCM_CUDA(c, cudaMemcpyAsync(pp, tv->params, R * sizeof(tcm_replica_params), cudaMemcpyHostToDevice, s));
+        t.offset = (const uint64_t*)o;
+        t.arrival = (const uint64_t*)a;
+        t.footprint = (const uint32_t*)f;
+        t.inl = (const uint32_t*)il;
+        t.out = (const uint16_t*)ou;
+        t.mod = (const uint8_t*)md;
+        t.params = (const tcm_replica_params*)pp;
+    } else {
+        uint64_t lastoff = 0;
+        TCM_CUDA(c, cudaMemcpyAsync(&lastoff, tv->req_offset + R, 8, cudaMemcpyDeviceToHost, s));
+        TCM_CUDA(c, cudaStreamSynchronize(s));
+        if (lastoff != N)
+            return fail(c, TCM_E_ARG, "req_offset[R] (%llu) != n_requests (%llu)",
+                        (unsigned long long)lastoff, (unsigned long long)N);
+        t.offset = tv->req_offset;
+        t.arrival = tv->arrival_us;
+        t.footprint = tv->footprint;
+        t.inl = tv->inline_us;
+        t.out = tv->out_tokens;
+        t.mod = tv->modality;
+        t.params = tv->params;
+    }
+
+    // results: caller DEVICE buffers, or device workspace (+ copy-back for HOST buffers)
+    c->host_results = rv && rv->mem == TCM_MEM_HOST;
+    if (c->host_results) c->host_res = *rv;
+    const bool dev_res = rv && rv->mem == TCM_MEM_DEVICE;
+    void* p;
+    if (dev_res && rv->admit_seq) t.admit_seq = rv->admit_seq;
+    else { if ((st = dalloc(c, &p, 4 * N))) return st; t.admit_seq = (uint32_t*)p; }
+    if (dev_res && rv->first_token_us) t.first_token = rv->first_token_us;
+    else { if ((st = dalloc(c, &p, 8 * N))) return st; t.first_token = (uint64_t*)p; }
+    if (dev_res && rv->done_us) t.done = rv->done_us;
+    else { if ((st = dalloc(c, &p, 8 * N))) return st; t.done = (uint64_t*)p; }
+
+    // workspace
+    if ((st = dalloc(c, &p, 4 * N))) return st;
+    t.link = (uint32_t*)p;
+    if ((st = dalloc(c, &p, (size_t)R * kCalSlots * 4))) return st;
+    t.cal = (uint32_t*)p;
+    if ((st = dalloc(c, &p, (size_t)R * kCalWords * 4))) return st;
+    t.occ = (uint32_t*)p;
+    if ((st = dalloc(c, &p, (size_t)R * sizeof(ReplicaState)))) return st;
+    t.state = (ReplicaState*)p;
+    if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
+        if ((st = dalloc(c, &p, N ? N : 1))) return st;
+        t.req_state = (uint8_t*)p;
+        if ((st = dalloc(c, &p, stepwise_extra_bytes(R)))) return st;
+        c->sw = stepwise_bind(p, R);
+    }
+
+    TCM_CUDA(c, cudaMemsetAsync(t.cal, 0xFF, (size_t)R * kCalSlots * 4, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.occ, 0, (size_t)R * kCalWords * 4, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.first_token, 0, 8 * N, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.done, 0, 8 * N, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.admit_seq, 0xFF, 4 * N, s));
+    if (t.req_state) TCM_CUDA(c, cudaMemsetAsync(t.req_state, 0, N ? N : 1, s));
+    launch_init(t, s);
+    c->launches++;
+
+    // validate on the device (R18)
+    uint32_t hv[2] = {0, 0xFFFFFFFFu};
+    TCM_CUDA(c, cudaMemcpyAsync(c->d_val, hv, 8, cudaMemcpyHostToDevice, s));
+    launch_validate(t, c->d_val, s);
+    c->launches++;
+    TCM_CUDA(c, cudaGetLastError());
+    TCM_CUDA(c, cudaMemcpyAsync(hv, c->d_val, 8, cudaMemcpyDeviceToHost, s));
+    TCM_CUDA(c, cudaStreamSynchronize(s));
+    if (hv[0] == ST_CAPACITY)
+        return fail(c, TCM_E_CAPACITY, "replica %u: a footprint exceeds kv_capacity (R18)", hv[1]);
+    if (hv[0] != ST_OK)
+        return fail(c, TCM_E_ARG, "replica %u: malformed trace or params (footprint/out/modality/"
+                    "arrival order/policy/budget/kv/alpha)", hv[1]);
+    c->t = t;
+    c->loaded = true;
+    c->err.clear();
+    return TCM_OK;
+}
+
+tcm_status tcm_step(tcm_ctx* c, uint32_t max_iterations, uint32_t* active_replicas) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_step before tcm_load_trace");
+    uint32_t active = 0;
+    tcm_status st = run_engine(c, max_iterations, &active);
+    if (st != TCM_OK) return st;
+    if ((st = copy_results_to_host(c)) != TCM_OK) return st;
+    TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    if (active_replicas) *active_replicas = active;
+    return TCM_OK;
+}
+
+tcm_status tcm_run(tcm_ctx* c) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_run before tcm_load_trace");
+    uint32_t active = 1;
+    while (active > 0) {
+        tcm_status st = run_engine(c, 0xFFFFFFFFu, &active);
+        if (st != TCM_OK) return st;
+    }
+    unsigned long long h[kAccN];
+    tcm_status st = reduce_stats(c, h);
+    if (st != TCM_OK) return st;
+    if ((st = copy_results_to_host(c)) != TCM_OK) return st;
+    TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    if (h[kAccBadStatus] != 0)
+        return fail(c, TCM_E_REPLICA, "replica %llu reported status %llu (deadlock assertion)",
+                    h[kAccBadReplica], h[kAccBadStatus]);
+    return TCM_OK;
+}
+
+tcm_status tcm_stats(tcm_ctx* c, tcm_stats_host* out, int64_t* dev_hist, int64_t* dev_cnt) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_stats before tcm_load_trace");
+    unsigned long long h[kAccN];
+    tcm_status st = reduce_stats(c, h);
+    if (st != TCM_OK) return st;
+    if (out) {
+        out->iterations = h[kAccIter];
+        out->decisions = h[kAccDecisions];
+        out->ff_iterations = h[kAccFF];
+        out->idle_jumps = h[kAccIdle];
+        out->sum_pending = h[kAccSumPending];
+        out->max_pending = h[kAccMaxPending];
+        out->requests_done = h[kAccDone];
+        out->replicas_done = h[kAccReplicasDone];
+        out->replicas_active = h[kAccReplicasActive];
+        out->first_bad_replica = h[kAccBadStatus] ? (int32_t)h[kAccBadReplica] : -1;
+        out->first_bad_status = (int32_t)h[kAccBadStatus];
+    }
+    if (dev_hist || dev_cnt) {
+        if (h[kAccReplicasActive] != 0)
+            return fail(c, TCM_E_STATE, "aggregation needs every replica finished (%llu active)",
+                        h[kAccReplicasActive]);
+        if (!dev_hist || !dev_cnt) return fail(c, TCM_E_ARG, "dev_hist and dev_cnt go together");
+        const size_t hb = (size_t)c->m.n_cells * kGroups * kHistBins * 8;
+        const size_t cb = (size_t)c->m.n_cells * kGroups * kNcnt * 8;
+        TCM_CUDA(c, cudaMemsetAsync(dev_hist, 0, hb, c->s));
+        TCM_CUDA(c, cudaMemsetAsync(dev_cnt, 0, cb, c->s));
+        launch_aggregate(c->m, c->t, reinterpret_cast<unsigned long long*>(dev_hist),
+                         reinterpret_cast<unsigned long long*>(dev_cnt), c->s);
+        c->launches++;
+        TCM_CUDA(c, cudaGetLastError());
+        TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    }
+    if (out) out->kernel_launches = c->launches;
+    return TCM_OK;
+}
+
+void tcm_destroy(tcm_ctx* c) {
+    if (!c) return;
+    free_allocs(c);
+    cudaFree(c->d_active);
+    cudaFree(c->d_acc);
+    cudaFree(c->d_val);
+    delete c;
+}
+
+const char* tcm_last_error(const tcm_ctx* c) {
+    return c ? c->err.c_str() : g_err.c_str();
+}
+
+size_t tcm_workspace_bytes(const tcm_config* cfg, uint32_t n_replicas, uint64_t n_requests, int host_mirror) {
+    return ws_bytes(cfg, n_replicas, n_requests, host_mirror);
+}
+
+tcm_status tcm_generate_trace(const tcm_gen_replica* reps, uint32_t R, const uint64_t* off,
+                              uint64_t* arrival, uint32_t* footprint, uint32_t* inl, uint16_t* out,
+                              uint8_t* mod, void* stream) {
+    if (!reps || !off || R == 0) return fail(nullptr, TCM_E_ARG, "bad generator arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    uint32_t* bad = nullptr;
+    cudaError_t e = cudaMalloc(&bad, 4);
+    if (e != cudaSuccess) return fail(nullptr, TCM_E_CUDA, "cudaMalloc: %s", cudaGetErrorString(e));
+    uint32_t hb = 0;
+    cudaMemsetAsync(bad, 0, 4, s);
+    launch_generate(reps, R, off, arrival, footprint, inl, out, mod, bad, s);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(bad);
+    if (e != cudaSuccess) return fail(nullptr, TCM_E_CUDA, "generator: %s", cudaGetErrorString(e));
+    if (hb) return fail(nullptr, TCM_E_ARG, "req_offset does not match n_requests");
+    return TCM_OK;
+}
+
+tcm_status tcm_k1_eval(const tcm_config* cfg, const uint8_t* cls, const uint64_t* w, const double* alpha,
+                       double* outp, uint64_t n, void* stream) {
+    tcm_status st = validate_config(cfg);
+    if (st != TCM_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    launch_k1_eval(to_model(*cfg), cls, w, alpha, outp, n, s);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(nullptr, TCM_E_CUDA, "k1_eval: %s", cudaGetErrorString(e));
+    return TCM_OK;
+}
+
+tcm_status tcm_k1_audit(const tcm_config* cfg, uint32_t cls, double alpha, uint64_t lo, uint64_t hi,
+                        uint64_t* first, void* stream) {
+    tcm_status st = validate_config(cfg);
+    if (st != TCM_OK) return st;
+    if (cls > 2 || hi <= lo || !first) return fail(nullptr, TCM_E_ARG, "bad audit arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(first, 0xFF, 8, s);
+    if (e == cudaSuccess) {
+        launch_k1_audit(to_model(*cfg), cls, alpha, lo, hi, reinterpret_cast<unsigned long long*>(first), s);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(nullptr, TCM_E_CUDA, "k1_audit: %s", cudaGetErrorString(e));
+    return TCM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,291 @@
+// tcm_aux.cu -- libtcm's non-step kernels: replica init, trace validation, work-counter
+// reduction, a6 aggregation (histograms + SLO counters), device trace generation, and the
+// K1 evaluation / monotonicity audit.
+#include "tcm_aux.cuh"
+#include "tcm_k1.cuh"
+#include "../../tracegen/tcm_tracegen.h"
+
+namespace tcm {
+
+// ---------------------------------------------------------------------------------------
+// Initial replica state: clock 0, all KV free, empty queues (SPEC.md:455 start of run).
+__global__ void k_init(TraceDev t) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= t.R) return;
+    ReplicaState st;
+    st.clock = 0;
+    st.kv_free = t.params[r].kv_capacity;
+    st.iter = 0;
+    st.nxt = 0;
+    st.seq = 0;
+    st.n_dec = 0;
+    st.n_pend = 0;
+    for (int c = 0; c < 3; ++c) {
+        st.head[c] = NIL;
+        st.tail[c] = NIL;
+        st.rem[c] = 0;
+    }
+    st.flags = 0;
+    st.status = ST_OK;
+    st.max_pending = 0;
+    st.decisions = 0;
+    st.sum_pending = 0;
+    st.ff_iters = 0;
+    st.idle_jumps = 0;
+    st.done_count = 0;
+    st.pad = 0;
+    t.state[r] = st;
+}
+
+// ---------------------------------------------------------------------------------------
+// Validation: one warp per replica, lanes stride its requests (coalesced).
+// v[0] = worst status code (max), v[1] = first bad replica (min).
+__global__ void k_validate(TraceDev t, uint32_t* v) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp >= t.R) return;
+    const uint32_t r = warp;
+    const tcm_replica_params p = t.params[r];
+    const uint64_t a = t.offset[r], b = t.offset[r + 1];
+    uint32_t bad = ST_OK;
+    if (b < a || b > t.N || b - a >= 0xFFFFFFFFull) bad = ST_BAD_INPUT;
+    if (p.policy > TCM_POLICY_TCM || p.chunk_budget == 0 || p.kv_capacity == 0 ||
+        p.kv_capacity > 0xFFFFFFFFull || !(p.aging_alpha >= 0.0) || p.reserved != 0)
+        bad = ST_BAD_INPUT;
+    if (bad == ST_OK) {
+        for (uint64_t i = a + lane; i < b; i += 32) {
+            const uint32_t f = t.footprint[i];
+            const uint32_t o = t.out[i];
+            if (f == 0 || o == 0 || o > kCalSlots || t.mod[i] > 2) bad = bad > ST_BAD_INPUT ? bad : ST_BAD_INPUT;
+            if (i > a && t.arrival[i] < t.arrival[i - 1]) bad = bad > ST_BAD_INPUT ? bad : ST_BAD_INPUT;
+            if ((uint64_t)f > p.kv_capacity) bad = ST_CAPACITY;
+        }
+    }
+    // ST_BAD_INPUT (2) vs ST_CAPACITY (3): report the larger code
+    const uint32_t worst = __reduce_max_sync(0xFFFFFFFFu, bad);
+    if (lane == 0 && worst != ST_OK) {
+        atomicMax(&v[0], worst);
+        atomicMin(&v[1], r);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Work counters: one thread per replica, warp-reduced, one atomic per warp and field.
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    return x;
+}
+
+__global__ void k_reduce(TraceDev t, unsigned long long* acc /* [kAccN] */) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    ReplicaState st;
+    bool live = r < t.R;
+    uint64_t v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t mx = 0;
+    if (live) {
+        st = t.state[r];
+        v[0] = st.iter;
+        v[1] = st.decisions;
+        v[2] = st.ff_iters;
+        v[3] = st.idle_jumps;
+        v[4] = st.sum_pending;
+        v[5] = st.done_count;
+        v[6] = (st.flags & FLAG_FINISHED) ? 1 : 0;
+        v[7] = (st.flags & FLAG_FINISHED) ? 0 : 1;
+        v[8] = 0;
+        mx = st.max_pending;
+        if (st.status != ST_OK) {
+            atomicMin(reinterpret_cast<unsigned long long*>(&acc[kAccBadReplica]), (unsigned long long)r);
+            atomicMax(reinterpret_cast<unsigned long long*>(&acc[kAccBadStatus]), (unsigned long long)st.status);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = warp_sum64(v[k]);
+    mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (v[k]) atomicAdd(&acc[k], (unsigned long long)v[k]);
+        atomicMax(&acc[kAccMaxPending], (unsigned long long)mx);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// a6 aggregation: warp per replica; per lane per-group
+// counters, warp-reduced; histogram bins by atomics.
+__device__ __forceinline__ uint32_t ttft_bucket(uint64_t t) {
+    if (t < 16) return (uint32_t)t;
+    const uint32_t e = 63u - (uint32_t)__clzll((long long)t);
+    return 16u + 8u * (e - 4u) + (uint32_t)((t >> (e - 3u)) & 7u);
+}
+
+__global__ void k_aggregate(ModelConst m, TraceDev t, unsigned long long* hist, unsigned long long* cnt) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp >= t.R) return;
+    const uint32_t r = warp;
+    const tcm_replica_params p = t.params[r];
+    const uint64_t a = t.offset[r], b = t.offset[r + 1];
+    const uint64_t B = p.chunk_budget;
+    uint64_t c[3][kNcnt];
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+#pragma unroll
+        for (int k = 0; k < (int)kNcnt; ++k) c[g][k] = 0;
+    unsigned long long* H = hist + (size_t)p.cell_id * kGroups * kHistBins;
+    for (uint64_t i = a + lane; i < b; i += 32) {
+        const uint32_t f = t.footprint[i];
+        const uint32_t o = t.out[i];
+        const int g = classify(m, t.mod[i], f);
+        const uint64_t arr = t.arrival[i];
+        const uint64_t ttft = t.first_token[i] - arr;
+        const uint64_t e2e = t.done[i] - arr;
+        const uint64_t iso = (uint64_t)t.inl[i] + ((uint64_t)f + B - 1) / B * m.c0 + m.cp * f +
+                             (uint64_t)(o - 1) * (m.c0 + m.cd);
+        const uint64_t lhs = e2e * m.slo_den, rhs = iso * m.slo_num;
+        const bool viol = lhs > rhs;
+        const uint32_t bk = ttft_bucket(ttft);
+        atomicAdd(&H[(size_t)g * kHistBins + bk], 1ull);
+        atomicAdd(&H[(size_t)3 * kHistBins + bk], 1ull);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (q == g) {
+                c[q][0] += 1;
+                c[q][1] += ttft;
+                c[q][2] += e2e;
+                c[q][3] += viol ? 1 : 0;
+                c[q][4] += viol ? lhs - rhs : 0;
+                c[q][5] += e2e / o;
+            }
+        }
+    }
+    unsigned long long* C = cnt + (size_t)p.cell_id * kGroups * kNcnt;
+#pragma unroll
+    for (int k = 0; k < (int)kNcnt; ++k) {
+        uint64_t all = 0;
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+            const uint64_t s = warp_sum64(c[g][k]);
+            all += s;
+            if (lane == 0 && s) atomicAdd(&C[g * kNcnt + k], (unsigned long long)s);
+        }
+        if (lane == 0 && all) atomicAdd(&C[3 * kNcnt + k], (unsigned long long)all);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Device trace generation (bit-identical to tracegen/ on the host): warp per replica,
+// 32 requests per round, gap prefix sum by warp scan, coalesced SoA stores.
+__global__ void k_generate(const tg_replica* reps, uint32_t R, const uint64_t* off, uint64_t* arrival,
+                           uint32_t* footprint, uint32_t* inl, uint16_t* out, uint8_t* mod, uint32_t* bad) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp >= R) return;
+    const tg_replica rp = reps[warp];
+    const uint64_t base = off[warp];
+    if (off[warp + 1] - base != rp.n_requests) {
+        if (lane == 0) atomicExch(bad, 1u);
+        return;
+    }
+    uint64_t carry = 0;
+    for (uint32_t i0 = 0; i0 < rp.n_requests; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        tg_request q;
+        uint64_t g = 0;
+        if (i < rp.n_requests) {
+            q = tg_draw(&rp, i);
+            g = i == 0 ? 0 : q.gap_us;
+        }
+        uint64_t s = g;                                  // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+            if (lane >= (uint32_t)o) s += y;
+        }
+        if (i < rp.n_requests) {
+            arrival[base + i] = carry + s;
+            footprint[base + i] = q.footprint;
+            inl[base + i] = q.inline_us;
+            out[base + i] = q.out_tokens;
+            mod[base + i] = q.modality;
+        }
+        carry += __shfl_sync(0xFFFFFFFFu, s, 31);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1 diagnostics.
+__global__ void k_k1_eval(ModelConst m, const uint8_t* cls, const uint64_t* w, const double* alpha,
+                          double* outp, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const int c = cls[i];
+        const K1Class kc = k1_class(m.S[c], m.k[c], m.p[c], alpha[i]);
+        outp[i] = k1_priority(kc, w[i]);
+    }
+}
+
+// Each thread audits a contiguous chunk [w0, w0 + chunk] of adjacent pairs.
+__global__ void k_k1_audit(ModelConst m, uint32_t c, double alpha, uint64_t lo, uint64_t hi, uint64_t chunk,
+                           unsigned long long* first) {
+    const K1Class kc = k1_class(m.S[c], m.k[c], m.p[c], alpha);
+    const uint64_t nchunks = (hi - lo + chunk - 1) / chunk;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nchunks;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w0 = lo + q * chunk;
+        uint64_t w1 = w0 + chunk;
+        if (w1 > hi) w1 = hi;
+        uint64_t prev = k1_key(kc, w0);
+        for (uint64_t w = w0 + 1; w <= w1; ++w) {
+            const uint64_t k = k1_key(kc, w);
+            if (k < prev) {
+                atomicMin(first, (unsigned long long)(w - 1));
+                break;
+            }
+            prev = k;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+void launch_init(const TraceDev& t, cudaStream_t s) {
+    k_init<<<(t.R + 127) / 128, 128, 0, s>>>(t);
+}
+void launch_validate(const TraceDev& t, uint32_t* v, cudaStream_t s) {
+    const uint64_t threads = (uint64_t)t.R * 32;
+    k_validate<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(t, v);
+}
+void launch_reduce(const TraceDev& t, unsigned long long* acc, cudaStream_t s) {
+    k_reduce<<<(t.R + 255) / 256, 256, 0, s>>>(t, acc);
+}
+void launch_aggregate(const ModelConst& m, const TraceDev& t, unsigned long long* hist,
+                      unsigned long long* cnt, cudaStream_t s) {
+    const uint64_t threads = (uint64_t)t.R * 32;
+    k_aggregate<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(m, t, hist, cnt);
+}
+void launch_generate(const void* reps, uint32_t R, const uint64_t* off, uint64_t* arrival,
+                     uint32_t* footprint, uint32_t* inl, uint16_t* out, uint8_t* mod, uint32_t* bad,
+                     cudaStream_t s) {
+    const uint64_t threads = (uint64_t)R * 32;
+    k_generate<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const tg_replica*>(reps), R, off, arrival, footprint, inl, out, mod, bad);
+}
+void launch_k1_eval(const ModelConst& m, const uint8_t* cls, const uint64_t* w, const double* alpha,
+                    double* outp, uint64_t n, cudaStream_t s) {
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks == 0) blocks = 1;
+    k_k1_eval<<<(uint32_t)blocks, 256, 0, s>>>(m, cls, w, alpha, outp, n);
+}
+void launch_k1_audit(const ModelConst& m, uint32_t c, double alpha, uint64_t lo, uint64_t hi,
+                     unsigned long long* first, cudaStream_t s) {
+    const uint64_t chunk = 1024;
+    uint64_t nchunks = (hi - lo + chunk - 1) / chunk;
+    uint64_t blocks = (nchunks + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks == 0) blocks = 1;
+    k_k1_audit<<<(uint32_t)blocks, 256, 0, s>>>(m, c, alpha, lo, hi, chunk, first);
+}
+
+}  // namespace tcm

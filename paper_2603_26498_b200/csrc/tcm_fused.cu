@@ -1,0 +1,287 @@
+// tcm_fused.cu -- TCM_ENGINE_FUSED: the whole per-iteration scheduling step (SURVEY.md 8(a)
+// rows a1-a5) for one replica, run by one persistent thread with the replica state in
+// registers.
+//
+// a3 is computed as the exact 3-way merge of the class-FIFO heads:
+//   Lemma L1: within class c every request shares (S_c, k_c, p_c) and K1 is
+//   non-decreasing in the waiting time, so the (key desc, arrival asc, id asc) order restricted
+//   to class c is arrival order -- the paper's "FCFS within each queue".
+//   The global order is therefore the merge of the three queue heads, and each decision
+//   keys only the <= 3 + admitted candidates it actually visits.
+//   Lemma L2: only a queue head can be partially prefilled, so per-request mutable state
+//   collapses to head_rem[3] / head-admitted bits in ReplicaState.
+//   Lemma L3: with nothing pending, consecutive iterations are identical until the next
+//   calendar event or arrival, so they are fast-forwarded in closed form (integer math).
+#include "tcm_internal.cuh"
+#include "tcm_k1.cuh"
+
+namespace tcm {
+
+namespace {
+
+struct Cal {
+    uint32_t* cal;
+    uint32_t* occ;
+};
+
+__device__ __forceinline__ void cal_insert(const Cal& c, uint32_t* link, uint32_t slot, uint32_t i) {
+    link[i] = c.cal[slot];
+    c.cal[slot] = i;
+    c.occ[slot >> 5] |= 1u << (slot & 31);
+}
+
+// Step 9 for iteration `iter`: every request whose last decode token is
+// produced in this iteration completes now and releases its KV (R7).
+__device__ __forceinline__ void cal_process(const Cal& c, uint32_t* link, uint64_t iter, uint64_t clock,
+                                            const uint32_t* fp, uint64_t* done, ReplicaState& st) {
+    const uint32_t s = (uint32_t)(iter & (kCalSlots - 1));
+    const uint32_t bit = 1u << (s & 31);
+    const uint32_t w = c.occ[s >> 5];
+    if (!(w & bit)) return;
+    uint32_t i = c.cal[s];
+    while (i != NIL) {
+        const uint32_t ni = link[i];
+        done[i] = clock;
+        st.kv_free += fp[i];
+        st.n_dec--;
+        st.done_count++;
+        i = ni;
+    }
+    c.cal[s] = NIL;
+    c.occ[s >> 5] = w & ~bit;
+}
+
+// Iteration number of the next occupied calendar slot after `iter` (one exists when n_dec > 0).
+__device__ __forceinline__ uint64_t cal_next(const Cal& c, uint64_t iter) {
+    const uint32_t s0 = (uint32_t)((iter + 1) & (kCalSlots - 1));
+    uint32_t wi = s0 >> 5;
+    uint32_t w = c.occ[wi] & (~0u << (s0 & 31));
+    uint32_t dist = 0u - (s0 & 31);
+    while (w == 0) {
+        wi = (wi + 1) & (kCalWords - 1);
+        dist += 32;
+        w = c.occ[wi];
+    }
+    return iter + 1 + (uint64_t)(dist + (uint32_t)(__ffs(w) - 1));
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t max_iters,
+                                              uint32_t* active) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= t.R) return;
+    ReplicaState st = t.state[r];
+    if (st.flags & FLAG_FINISHED) return;
+
+    const tcm_replica_params prm = t.params[r];
+    const uint64_t base = t.offset[r];
+    const uint32_t n = (uint32_t)(t.offset[r + 1] - base);
+    const uint64_t* __restrict__ arr = t.arrival + base;
+    const uint32_t* __restrict__ fp = t.footprint + base;
+    const uint32_t* __restrict__ inl = t.inl + base;
+    const uint16_t* __restrict__ out = t.out + base;
+    const uint8_t* __restrict__ mod = t.mod + base;
+    uint32_t* admit = t.admit_seq + base;
+    uint64_t* first = t.first_token + base;
+    uint64_t* done = t.done + base;
+    uint32_t* link = t.link + base;
+    const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};
+
+    const bool prio = prm.policy == TCM_POLICY_TCM;
+    const uint32_t B = prm.chunk_budget;
+    K1Class kc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) kc[c] = k1_class(m.S[c], m.k[c], m.p[c], prm.aging_alpha);
+
+    // Cached arrival / footprint of each queue head.
+    uint64_t harr[3];
+    uint32_t hf[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        harr[c] = st.head[c] != NIL ? arr[st.head[c]] : 0;
+        hf[c] = st.head[c] != NIL ? fp[st.head[c]] : 0;
+    }
+    uint64_t next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
+    uint32_t budget = max_iters;
+
+    for (;;) {
+        // ---- a1: ingest arrivals <= clock; classify; append to the class FIFO
+        while (next_arr <= st.clock) {
+            const uint32_t i = st.nxt;
+            const uint32_t f = fp[i];
+            const int q = prio ? classify(m, mod[i], f) : 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (c == q) {
+                    if (st.head[c] == NIL) {
+                        st.head[c] = i;
+                        st.rem[c] = f;
+                        st.flags &= ~(1u << c);
+                        harr[c] = next_arr;
+                        hf[c] = f;
+                    } else {
+                        link[st.tail[c]] = i;
+                    }
+                    st.tail[c] = i;
+                }
+            }
+            st.n_pend++;
+            st.nxt++;
+            next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
+        }
+
+        if (st.n_pend == 0) {
+            if (st.n_dec == 0) {
+                if (st.nxt == n) {                      // every request served
+                    st.flags |= FLAG_FINISHED;
+                    break;
+                }
+                st.clock = next_arr;                    // R15 idle jump (not an iteration)
+                st.idle_jumps++;
+                continue;
+            }
+            if (budget == 0) break;
+            // ---- Lemma L3: decode-only iterations until the next finish or arrival
+            const uint64_t F = cal_next(cal, st.iter);
+            const uint64_t dt = m.c0 + m.cd * st.n_dec;
+            uint64_t j = F - st.iter;
+            if (next_arr != ~0ull) {
+                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+                j = ja < j ? ja : j;
+            }
+            j = j < budget ? j : budget;
+            st.clock += j * dt;
+            st.iter += j;
+            st.ff_iters += j;
+            budget -= (uint32_t)j;
+            if (st.iter == F) cal_process(cal, link, st.iter, st.clock, fp, done, st);
+            continue;
+        }
+        if (budget == 0) break;
+
+        // ---- a2 + a3 + a4: merge the class-FIFO heads by key, scan under token/KV budgets
+        uint32_t left = B > st.n_dec ? B - st.n_dec : 0;   // R8
+        uint64_t tok = 0, inl_sum = 0;
+        bool blocked = false;                               // R6
+        uint32_t cur[3], crem[3], cf[3];
+        uint64_t carr[3], key[3];
+        bool cres[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            cur[c] = st.head[c];
+            crem[c] = st.rem[c];
+            carr[c] = harr[c];
+            cf[c] = hf[c];
+            cres[c] = (st.flags >> c) & 1u;
+            key[c] = (prio && cur[c] != NIL) ? k1_key(kc[c], st.clock - carr[c]) : 0;
+        }
+        while (left > 0) {
+            int best = -1;
+            uint64_t bk = 0, ba = 0;
+            uint32_t bi = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (cur[c] != NIL && (!blocked || cres[c])) {
+                    const bool better = best < 0 || key[c] > bk ||
+                                        (key[c] == bk && (carr[c] < ba || (carr[c] == ba && cur[c] < bi)));
+                    if (better) {
+                        best = c;
+                        bk = key[c];
+                        ba = carr[c];
+                        bi = cur[c];
+                    }
+                }
+            }
+            if (best < 0) break;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (c == best) {
+                    const uint32_t i = cur[c];
+                    bool go = true;
+                    if (!cres[c]) {
+                        if ((uint64_t)cf[c] > st.kv_free) {
+                            blocked = true;                 // first misfit stops new admits
+                            go = false;
+                        } else {
+                            st.kv_free -= cf[c];            // R7 reserve the full footprint
+                            admit[i] = st.seq++;
+                            inl_sum += inl[i];              // R10
+                            cres[c] = true;
+                        }
+                    }
+                    if (go) {
+                        const uint32_t ch = crem[c] < left ? crem[c] : left;
+                        crem[c] -= ch;
+                        left -= ch;
+                        tok += ch;
+                        if (crem[c] == 0) {                 // prefill complete: next in FIFO
+                            if (i == st.tail[c]) {
+                                cur[c] = NIL;
+                            } else {
+                                const uint32_t ni = link[i];
+                                cur[c] = ni;
+                                carr[c] = arr[ni];
+                                cf[c] = fp[ni];
+                                crem[c] = cf[c];
+                                cres[c] = false;
+                                if (prio) key[c] = k1_key(kc[c], st.clock - carr[c]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (tok == 0 && st.n_dec == 0) {                    // unreachable under R6
+            st.status = ST_DEADLOCK;
+            st.flags |= FLAG_FINISHED;
+            break;
+        }
+
+        // ---- a5: iteration cost, clock, decode calendar, first tokens (R12)
+        st.clock += m.c0 + m.cp * tok + m.cd * (uint64_t)st.n_dec + inl_sum;
+        st.iter++;
+        st.decisions++;
+        st.sum_pending += st.n_pend;
+        st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
+        budget--;
+        cal_process(cal, link, st.iter, st.clock, fp, done, st);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            uint32_t i = st.head[c];
+            while (i != cur[c]) {
+                const uint32_t ni = (i == st.tail[c]) ? NIL : link[i];
+                first[i] = st.clock;
+                st.n_pend--;
+                const uint32_t o = out[i];
+                if (o == 1) {
+                    done[i] = st.clock;
+                    st.kv_free += fp[i];
+                    st.done_count++;
+                } else {
+                    cal_insert(cal, link, (uint32_t)((st.iter + o - 1) & (kCalSlots - 1)), i);
+                    st.n_dec++;
+                }
+                i = ni;
+            }
+            st.head[c] = cur[c];
+            if (cur[c] == NIL) st.tail[c] = NIL;
+            st.rem[c] = crem[c];
+            st.flags = cres[c] ? (st.flags | (1u << c)) : (st.flags & ~(1u << c));
+            harr[c] = carr[c];
+            hf[c] = cf[c];
+        }
+    }
+
+    t.state[r] = st;
+    if (!(st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
+}
+
+void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, uint32_t* d_active,
+                  cudaStream_t s) {
+    const uint32_t threads = 64;
+    const uint32_t blocks = (t.R + threads - 1) / threads;
+    k_fused<<<blocks, threads, 0, s>>>(m, t, max_iters, d_active);
+}
+
+}  // namespace tcm

@@ -1,0 +1,86 @@
+// tcm_internal.cuh -- device-side data layout shared by libtcm's kernels (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tcm.h"
+
+namespace tcm {
+
+constexpr uint32_t NIL = 0xFFFFFFFFu;
+constexpr uint32_t kCalSlots = 2048;      // decode calendar ring: out <= 2048 (R23)
+constexpr uint32_t kCalWords = kCalSlots / 32;
+constexpr uint32_t kHistBins = 496;
+constexpr uint32_t kGroups = 4;           // M, C, T, all
+constexpr uint32_t kNcnt = 6;
+
+// Replica status codes (device), mirrored in tcm_stats_host.first_bad_status.
+enum : uint32_t { ST_OK = 0, ST_DEADLOCK = 1, ST_BAD_INPUT = 2, ST_CAPACITY = 3 };
+
+// Per-replica mutable state.  Between launches it lives in HBM (128 B, one line);
+// inside the fused kernel it lives in registers.
+struct __align__(16) ReplicaState {
+    uint64_t clock;          // integer-us engine clock (R9)
+    uint64_t kv_free;        // free KV tokens (R7: reserve-on-admit)
+    uint64_t iter;           // iterations so far (calendar index)
+    uint32_t nxt;            // next request (local id) to ingest
+    uint32_t seq;            // next admit_seq
+    uint32_t n_dec;          // decoding sequences
+    uint32_t n_pend;         // pending (waiting + partial) requests
+    uint32_t head[3];        // class-queue heads (local ids, NIL if empty)
+    uint32_t tail[3];        // class-queue tails
+    uint32_t rem[3];         // remaining prefill tokens of head[c]
+    uint32_t flags;          // bit c: head[c] admitted (KV reserved); bit 8: finished
+    uint32_t status;         // ST_*
+    uint32_t max_pending;
+    uint64_t decisions;      // R17
+    uint64_t sum_pending;
+    uint64_t ff_iters;
+    uint64_t idle_jumps;
+    uint32_t done_count;
+    uint32_t pad;
+};
+static_assert(sizeof(ReplicaState) == 128, "ReplicaState must be one 128-byte line");
+
+constexpr uint32_t FLAG_FINISHED = 1u << 8;
+
+// Model constants in the kernels' parameter space.
+struct ModelConst {
+    uint64_t c0, cp, cd;
+    double S[3], k[3], p[3];
+    uint32_t thr_mc[3], thr_ct[3];
+    uint32_t slo_num, slo_den;
+    uint32_t n_cells;
+};
+
+// Everything a kernel needs about the bound trace (device pointers).
+struct TraceDev {
+    uint32_t R;
+    uint64_t N;
+    const uint64_t* offset;
+    const uint64_t* arrival;
+    const uint32_t* footprint;
+    const uint32_t* inl;
+    const uint16_t* out;
+    const uint8_t* mod;
+    const tcm_replica_params* params;
+    uint32_t* admit_seq;
+    uint64_t* first_token;
+    uint64_t* done;
+    // workspace
+    uint32_t* link;          // [N] class-queue / calendar-slot intrusive next pointer
+    uint32_t* cal;           // [R * kCalSlots] calendar slot list heads
+    uint32_t* occ;           // [R * kCalWords] calendar occupancy bits
+    ReplicaState* state;     // [R]
+    uint8_t* req_state;      // [N] stepwise engine: per-request class / phase byte
+};
+
+__device__ __forceinline__ int classify(const ModelConst& m, uint32_t mod, uint32_t f) {
+    // R13: per-modality footprint thresholds (smart classifier).
+    return f < m.thr_mc[mod] ? 0 : (f < m.thr_ct[mod] ? 1 : 2);
+}
+
+void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, uint32_t* d_active,
+                  cudaStream_t s);
+
+}  // namespace tcm

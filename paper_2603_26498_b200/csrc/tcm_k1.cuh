@@ -1,0 +1,118 @@
+// tcm_k1.cuh -- device implementation of K1, the specified priority key.
+//
+// Priority_c = StaticPriority_c + (1 - e^{-k_c * waiting_time^{p_c}})
+// with waiting_time in seconds (R1), ordered by max(P, 1e-12) descending (R3).
+// Every operation is an explicitly rounded IEEE binary64 op (__dmul_rn/__dadd_rn/__fma_rn)
+// so the result is bit-identical to any conforming implementation of the spec text.
+// Written from DESIGN.md 4 independently of oracle/ (no shared code or headers).
+#pragma once
+#include <stdint.h>
+
+namespace tcm {
+
+// DESIGN.md "K1 constants", transcribed.
+__constant__ double kLnR[16] = {
+    0x1.f0p-1, 0x1.d4p-1, 0x1.bap-1, 0x1.a4p-1, 0x1.90p-1, 0x1.7ep-1, 0x1.6cp-1, 0x1.5cp-1,
+    0x1.4ep-1, 0x1.42p-1, 0x1.36p-1, 0x1.2ap-1, 0x1.20p-1, 0x1.16p-1, 0x1.0cp-1, 0x1.04p-1};
+__constant__ double kLnT[16] = {
+    0x1.0415d89e74444p-5, 0x1.700d30aeac0e1p-4, 0x1.2d1610c86813ap-3, 0x1.95a5adcf7017fp-3,
+    0x1.f991c6cb3b379p-3, 0x1.2bef07cdc9354p-2, 0x1.5d5bddf595f30p-2, 0x1.8b639a88b2df5p-2,
+    0x1.b56fa04462909p-2, 0x1.dae75484c9616p-2, 0x1.00e5ae5b207abp-1, 0x1.151c3f6f29612p-1,
+    0x1.269621134db92p-1, 0x1.38ae2171976e7p-1, 0x1.4b6fd6f970c1fp-1, 0x1.5af405c3649e0p-1};
+__constant__ double kExpT[16] = {
+    0x1p+0,               0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0, 0x1.2387a6e756238p+0,
+    0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,
+    0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0, 0x1.ea4afa2a490dap+0};
+
+constexpr double kLN2 = 0x1.62e42fefa39efp-1;
+constexpr double kInvLn2x16 = 0x1.71547652b82fep+4;
+constexpr double kLn2d16Hi = 0x1.62e42fee00000p-5;
+constexpr double kLn2d16Lo = 0x1.a39ef35793c76p-37;
+constexpr double kEps = 1e-12;
+
+// LN(v), v a positive normal double: steps LN.1-LN.6.
+__device__ __forceinline__ double k1_ln(double v) {
+    const uint64_t b = (uint64_t)__double_as_longlong(v);
+    const int e = (int)((b >> 52) & 0x7FF) - 1023;
+    const int j = (int)((b >> 48) & 0xF);
+    const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+    const double u = __fma_rn(m, kLnR[j], -1.0);
+    double q = 0x1.c71c71c71c71cp-4;                 // c9
+    q = __fma_rn(q, u, -0x1p-3);                     // c8
+    q = __fma_rn(q, u, 0x1.2492492492492p-3);        // c7
+    q = __fma_rn(q, u, -0x1.5555555555555p-3);       // c6
+    q = __fma_rn(q, u, 0x1.999999999999ap-3);        // c5
+    q = __fma_rn(q, u, -0x1p-2);                     // c4
+    q = __fma_rn(q, u, 0x1.5555555555555p-2);        // c3
+    q = __fma_rn(q, u, -0x1p-1);                     // c2
+    q = __fma_rn(q, u, 0x1p+0);                      // c1
+    const double lnm = __dmul_rn(q, u);
+    const double t = __dadd_rn(kLnT[j], lnm);
+    return __fma_rn((double)e, kLN2, t);
+}
+
+// EXP(y): steps EXP.1-EXP.7.
+__device__ __forceinline__ double k1_exp(double y) {
+    if (y < -745.0) return 0.0;
+    if (y > 700.0) return __longlong_as_double(0x7FF0000000000000ll);
+    const double kf = rint(__dmul_rn(y, kInvLn2x16));
+    double r = __fma_rn(-kf, kLn2d16Hi, y);
+    r = __fma_rn(-kf, kLn2d16Lo, r);
+    double p = 0x1.6c16c16c16c17p-10;                // 1/6!
+    p = __fma_rn(p, r, 0x1.1111111111111p-7);        // 1/5!
+    p = __fma_rn(p, r, 0x1.5555555555555p-5);        // 1/4!
+    p = __fma_rn(p, r, 0x1.5555555555555p-3);        // 1/3!
+    p = __fma_rn(p, r, 0x1p-1);                      // 1/2!
+    p = __fma_rn(p, r, 0x1p+0);                      // 1/1!
+    p = __fma_rn(p, r, 0x1p+0);                      // 1/0!
+    const long long k = (long long)kf;
+    const long long j = k & 15;
+    const long long n = (k - j) / 16;
+    const double s = __dmul_rn(kExpT[j], p);
+    if (n < -1021) return 0.0;
+    const double res = __dmul_rn(s, __longlong_as_double((long long)((unsigned long long)(n + 1023) << 52)));
+    if (res < 0x1p-1022) return 0.0;
+    return res;
+}
+
+// Per (replica, class) constant: C_c = LN(alpha*k_c) - p_c * LN(10^6); zero rate if alpha*k_c is 0
+// or subnormal.
+struct K1Class {
+    double S, p, C;
+    bool zero;
+};
+
+__device__ __forceinline__ K1Class k1_class(double S, double k, double p, double alpha) {
+    K1Class kc;
+    kc.S = S;
+    kc.p = p;
+    const double a = __dmul_rn(alpha, k);
+    if (!(a >= 0x1p-1022)) {
+        kc.zero = true;
+        kc.C = 0.0;
+    } else {
+        kc.zero = false;
+        const double t = __dmul_rn(p, k1_ln(1000000.0));
+        kc.C = __dsub_rn(k1_ln(a), t);
+    }
+    return kc;
+}
+
+__device__ __forceinline__ double k1_priority(const K1Class& kc, uint64_t w) {
+    if (w == 0 || kc.zero) return kc.S;
+    const double L = k1_ln(__ull2double_rn(w));
+    const double y = __fma_rn(kc.p, L, kc.C);
+    const double x = k1_exp(y);
+    const double e = k1_exp(-x);
+    return __dadd_rn(kc.S, __dsub_rn(1.0, e));
+}
+
+// Key: bit pattern of max(P, 1e-12), compared as unsigned, larger first.
+__device__ __forceinline__ uint64_t k1_key(const K1Class& kc, uint64_t w) {
+    double P = k1_priority(kc, w);
+    P = P < kEps ? kEps : P;
+    return (uint64_t)__double_as_longlong(P);
+}
+
+}  // namespace tcm
