@@ -1,0 +1,434 @@
+#!/usr/bin/env python3
+"""Benchmark: TCM-Serve's per-iteration scheduling step as a trace-driven simulation on B200.
+
+Metric (BASELINE.json): scheduling decisions/s and simulated requests/s at 1/2/4/8 B200, with
+the HBM-roofline fraction.  Workload at N GPUs: the C4 memory-pressure sweep (video-heavy
+50/20/30 mix, KV {128k,64k,32k,16k} x lambda {0.5,1,2,4} x {FCFS,TCM}), 65,536 replicas x
+10,000 requests PER GPU (weak scaling: replicas are independent; rank k simulates global
+replicas k, k+N, ...).  One step = reset + tcm_run (rows a1-a5 to completion for every
+replica) + a6 aggregation (tcm_stats) + NCCL all-reduce of the int64 histograms (N > 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tcm|reference]
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the reference arm for
+this tier) on a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0           # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+
+# algorithmic bytes: fused engine per simulated request / per replica
+FUSED_BYTES_PER_REQ = 19 + 20 + 8 + 8     # trace read, results written, FIFO link w+r, calendar push+pop
+FUSED_BYTES_PER_REPLICA = 256 + 8192 + 256  # state r+w, calendar heads init, occupancy
+STEP_BYTES_PER_PENDING = 9                 # stepwise: arrival (8) + state byte (1) per pending key
+STEP_BYTES_PER_DECISION = 256              # replica state r+w
+
+
+def peak_hbm():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "tcm" else "gloo"
+        dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------------- oracle
+def _oracle_job(job):
+    import oracle as O
+    import tracegen as T
+    gen, pol, kv, alpha, budget, n = job
+    rep = np.array([gen], dtype=T.TG_REPLICA_DTYPE)
+    rep["n_requests"] = n
+    tr = T.generate(rep)
+    t0 = time.perf_counter()
+    r = O.simulate_trace(tr, 0, policy=pol, alpha=alpha, kv_capacity=kv, chunk_budget=budget)
+    dt = time.perf_counter() - t0
+    assert r.status == 0
+    return dt, n, r.counters["decisions"]
+
+
+def oracle_sample(sweep, budget_s=20.0, n_trunc=1000, max_jobs=None):
+    """Time the oracle (as it stands) on a bounded sample: every (R/64)-th replica of the sweep
+    truncated to its first n_trunc requests, one replica per process on the host cores."""
+    import multiprocessing as mp
+    R = sweep.n_replicas
+    step = max(1, R // 64)
+    idx = list(range(0, R, step))[: (max_jobs or 64)]
+    jobs = [(sweep.gen[i], int(sweep.params[i]["policy"]), int(sweep.params[i]["kv_capacity"]),
+             float(sweep.params[i]["aging_alpha"]), int(sweep.params[i]["chunk_budget"]), n_trunc) for i in idx]
+    cores = min(len(jobs), os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_oracle_job, jobs, chunksize=1)
+    wall = time.perf_counter() - t0
+    nreq = sum(r[1] for r in res)
+    ndec = sum(r[2] for r in res)
+    return {"wall_s": wall, "requests": nreq, "decisions": ndec, "cores": cores, "replicas": len(jobs),
+            "n_trunc": n_trunc}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2603_26498_b200 import workloads as W
+    sw = W.c4(0, 1, replicas_per_gpu=args.replicas, n_requests=args.requests)
+    for _ in range(args.warmup):
+        oracle_sample(sw, n_trunc=args.ref_requests, max_jobs=16)
+    tot_req = tot_dec = 0
+    tot_wall = 0.0
+    cores = 0
+    for _ in range(args.steps):
+        s = oracle_sample(sw, n_trunc=args.ref_requests, max_jobs=16)
+        tot_req += s["requests"]
+        tot_dec += s["decisions"]
+        tot_wall += s["wall_s"]
+        cores = s["cores"]
+    v = tot_req / tot_wall
+    sample = (f"16 replicas of C4 (every {max(1, sw.n_replicas // 64)}th), first {args.ref_requests} requests each, "
+              f"one oracle process per replica")
+    line = {
+        "impl": "reference", "metric": "simulated requests/sec (C4 memory-pressure sweep)", "value": v,
+        "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
+        "decisions_per_s": tot_dec / tot_wall,
+        "config": {"workload": "C4 memory-pressure sweep (bounded oracle sample)", "replicas": 16,
+                   "requests_per_replica": args.ref_requests},
+        "cpu_baseline": {"value": v, "unit": "requests/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ GPU
+def run_tcm(args, rank, world, local):
+    import torch
+    from paper_2603_26498_b200 import _build, tcm
+    from paper_2603_26498_b200 import workloads as W
+
+    _build.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    sw = W.c4(rank, world, replicas_per_gpu=args.replicas, n_requests=args.requests)
+    R, N = sw.n_replicas, sw.n_requests
+    with torch.cuda.stream(stream):
+        trace = tcm.generate_device(sw.gen, device=dev, stream=stream)
+        trace["params"] = torch.from_numpy(sw.params.view(np.uint8)).to(dev)
+        results = tcm.alloc_results(N, device=dev)
+    stream.synchronize()
+    cfg = tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells)
+    sim = tcm.Simulation(cfg, stream)
+    sim.load(trace, results)
+    hist = torch.zeros((sw.n_cells, tcm.GROUPS, tcm.HIST_BINS), dtype=torch.int64, device=dev)
+    cnt = torch.zeros((sw.n_cells, tcm.GROUPS, tcm.NCNT), dtype=torch.int64, device=dev)
+
+    def one_step():
+        sim.reset()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.run()
+        e1.record(stream)
+        tcm.tcm_stats(sim.ctx, hist, cnt)
+        if dist is not None:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(hist)
+                dist.all_reduce(cnt)
+        return e0, e1
+
+    for _ in range(args.warmup):
+        one_step()
+    stream.synchronize()
+    st0 = sim.stats()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    kern = []
+    for _ in range(args.steps):
+        kern.append(one_step())
+    t_end.record(stream)
+    stream.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    ms = t_start.elapsed_time(t_end)
+    run_ms = [a.elapsed_time(b) for a, b in kern]
+    st1 = sim.stats()
+    decisions = st1["decisions"] - 0  # counters reset each step: st1 holds the last step
+    launches_per_step = (st1["kernel_launches"] - st0["kernel_launches"]) / args.steps
+
+    # max over ranks of the device time; totals over ranks
+    tot = torch.tensor([float(N * args.steps), float(st1["decisions"] * args.steps),
+                        float(st1["iterations"] * args.steps)], dtype=torch.float64, device=dev)
+    mx = torch.tensor([ms, max(run_ms)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(tot)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    ms_max = float(mx[0])
+    req_s = float(tot[0]) / (ms_max / 1e3)
+    dec_s = float(tot[1]) / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (k_fused): algorithmic bytes per launch / launch time
+    peak, peak_kind = peak_hbm()
+    run_avg_ms = float(np.mean(run_ms))
+    alg_bytes = N * FUSED_BYTES_PER_REQ + R * FUSED_BYTES_PER_REPLICA
+    achieved = alg_bytes / (run_avg_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "fused_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_request")
+            traffic = traffic * N if traffic else None
+        except Exception:
+            traffic = None
+
+    out = {
+        "metric": "simulated requests/sec (C4 memory-pressure sweep); decisions/sec alongside",
+        "value": req_s, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
+        "decisions_per_s": dec_s,
+        "config": {"workload": f"C4 memory-pressure sweep: {args.replicas} replicas x {args.requests} requests per GPU "
+                               "(50/20/30 mix, KV 128k..16k x lambda 0.5..4 x FCFS/TCM), fused engine",
+                   "replicas_per_gpu": args.replicas, "requests_per_replica": args.requests,
+                   "requests_per_step": int(tot[0] / args.steps), "parallelism": f"replicas sharded x{world}",
+                   "l2": "inputs larger than L2 (trace %.1f GB per GPU)" % (N * 19 / 1e9)},
+        "roofline": {"kernel": "k_fused", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "note": "latency-bound per-replica chains; HBM is not the binding roof (DESIGN.md 7)"},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clocks,
+        "work": {"iterations_per_step": st1["iterations"], "decisions_per_step": st1["decisions"],
+                 "sum_pending_per_step": st1["sum_pending"], "ff_iterations": st1["ff_iterations"],
+                 "run_ms": run_ms},
+    }
+
+    # stepwise (paper-literal) per-step kernel on C2': its own HBM roofline
+    if not args.skip_step and rank == 0:
+        out["roofline_step"] = bench_stepwise(args, dev, stream)
+
+    # end-to-end through the C ABI with HOST buffers (H2D + run + D2H inside the timed region)
+    if not args.skip_e2e:
+        out["e2e"] = bench_e2e(args, sw, trace, dev, stream, dist, world)
+
+    if rank == 0 and not args.skip_cpu:
+        s = oracle_sample(sw, n_trunc=args.ref_requests, max_jobs=16)
+        out["cpu_baseline"] = {"value": s["requests"] / s["wall_s"], "unit": "requests/s", "cores": s["cores"],
+                               "kind": "oracle",
+                               "decisions_per_s": s["decisions"] / s["wall_s"],
+                               "sample": f"{s['replicas']} C4 replicas (every {max(1, R // 64)}th), first "
+                                         f"{s['n_trunc']} requests each, one oracle process per replica, "
+                                         f"{s['wall_s']:.1f} s wall"}
+    sim.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def bench_stepwise(args, dev, stream):
+    """One paper-literal step (a1-a5) over C2': 65,536 replicas x ~1k pending."""
+    import torch
+    import tracegen as T
+    from paper_2603_26498_b200 import tcm
+    from paper_2603_26498_b200 import workloads as W
+
+    sw = W.c2prime(replicas=args.step_replicas, pending=args.step_pending)
+    with torch.cuda.stream(stream):
+        tr = tcm.generate_device(sw.gen, device=dev, stream=stream)
+        first = tr["req_offset"][:-1].to(torch.int64)
+        tr["inline_us"].view(torch.int32)[first] = 60_000_000     # 60 s of encode time
+        tr["modality"][first] = 1
+        tr["footprint"].view(torch.int32)[first] = 800
+        tr["params"] = torch.from_numpy(sw.params.view(np.uint8)).to(dev)
+    stream.synchronize()
+    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE), stream)
+    sim.load(tr, None)
+    times, pend = [], []
+    for rep in range(args.step_reps):
+        sim.reset()
+        sim.step(1)                 # iteration 1: request 0 alone (60 s inline)
+        for it in range(args.step_iters):
+            s0 = sim.stats()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sim.step(1)
+            e1.record(stream)
+            stream.synchronize()
+            s1 = sim.stats()
+            if rep > 0:            # first repetition is warm-up
+                times.append(e0.elapsed_time(e1))
+                pend.append(s1["sum_pending"] - s0["sum_pending"])
+    sim.close()
+    peak, peak_kind = peak_hbm()
+    ms = float(np.mean(times))
+    bytes_per = float(np.mean(pend)) * STEP_BYTES_PER_PENDING + args.step_replicas * STEP_BYTES_PER_DECISION
+    achieved = bytes_per / (ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "step_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    return {"kernel": "k_step", "workload": f"C2': {args.step_replicas} replicas x {args.step_pending} pending, "
+            "one iteration (a1-a5), stepwise engine", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "ms_per_step": ms, "keys_per_step": float(np.mean(pend)),
+            "decisions_per_s": args.step_replicas / (ms / 1e3)}
+
+
+def bench_e2e(args, sw, trace, dev, stream, dist, world):
+    """Same metric through the C ABI with HOST (pinned) buffers: every step copies the trace in,
+    runs, copies per-request results back and reads the a6 counters."""
+    import torch
+    from paper_2603_26498_b200 import tcm
+    N = sw.n_requests
+    host = {}
+    for k in ("req_offset", "arrival_us", "footprint", "inline_us", "out_tokens", "modality", "params"):
+        t = trace[k].cpu().pin_memory()
+        host[k] = t
+    res = {"admit_seq": torch.empty(N, dtype=torch.uint32).pin_memory(),
+           "first_token_us": torch.empty(N, dtype=torch.uint64).pin_memory(),
+           "done_us": torch.empty(N, dtype=torch.uint64).pin_memory()}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = sum(v.numel() * v.element_size() for v in res.values())
+    cfg = tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells)
+    sim = tcm.Simulation(cfg, stream)
+    steps = max(1, min(args.steps, 2))
+
+    def step():
+        sim.load(host, res, mem=tcm.MEM_HOST)     # H2D inside the timed region
+        sim.run()                                 # results copied back (D2H) before returning
+        hist, cnt, _ = sim.aggregate(device=dev)
+        return cnt
+
+    step()                                        # warm-up
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    mx = torch.tensor([wall], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sim.close()
+    total_req = N * world * steps
+    return {"value": total_req / float(mx[0]), "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "note": "HOST pinned buffers through tcm_load_trace/tcm_run/tcm_stats; host wall clock, max over ranks"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["tcm", "reference"], default="tcm")
+    ap.add_argument("--replicas", type=int, default=65536, help="C4 replicas per GPU")
+    ap.add_argument("--requests", type=int, default=10_000)
+    ap.add_argument("--ref-requests", type=int, default=1000, help="oracle sample: requests per replica")
+    ap.add_argument("--step-replicas", type=int, default=65536)
+    ap.add_argument("--step-pending", type=int, default=1024)
+    ap.add_argument("--step-iters", type=int, default=4)
+    ap.add_argument("--step-reps", type=int, default=3)
+    ap.add_argument("--skip-step", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_tcm(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

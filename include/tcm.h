@@ -162,6 +162,11 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out);
 tcm_status tcm_load_trace(tcm_ctx* ctx, const tcm_trace_view* trace,
                           const tcm_results_view* results);
 
+/* Resets every replica of the bound trace to its initial state (clock 0, all KV free, no
+ * request admitted) without re-validating or re-copying the trace: device work only
+ * (memsets + one kernel), enqueued on the stream.  TCM_E_STATE before tcm_load_trace. */
+tcm_status tcm_reset(tcm_ctx* ctx);
+
 /* Advances every unfinished replica by at most max_iterations engine iterations (a
  * fast-forward counts all the iterations it covers; idle jumps count none).  Writes the
  * number of replicas still unfinished to *active_replicas (may be NULL).  HOST results

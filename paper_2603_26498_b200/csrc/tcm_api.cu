@@ -140,6 +140,28 @@ tcm_status reduce_stats(tcm_ctx* c, unsigned long long* h) {
     return TCM_OK;
 }
 
+// Initial state of every replica (clock 0, empty queues, all KV free).
+tcm_status reset_state(tcm_ctx* c) {
+    const TraceDev& t = c->t;
+    cudaStream_t s = c->s;
+    const uint32_t R = t.R;
+    const uint64_t N = t.N;
+    TCM_CUDA(c, cudaMemsetAsync(t.cal, 0xFF, (size_t)R * kCalSlots * 4, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.occ, 0, (size_t)R * kCalWords * 4, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.first_token, 0, 8 * N, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.done, 0, 8 * N, s));
+    TCM_CUDA(c, cudaMemsetAsync(t.admit_seq, 0xFF, 4 * N, s));
+    if (t.req_state) TCM_CUDA(c, cudaMemsetAsync(t.req_state, 0, N ? N : 1, s));
+    launch_init(t, s);
+    c->launches++;
+    if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
+        stepwise_init(t, s);
+        c->launches++;
+    }
+    TCM_CUDA(c, cudaGetLastError());
+    return TCM_OK;
+}
+
 tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
     TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
     if (c->cfg.engine == TCM_ENGINE_FUSED) {
@@ -267,18 +289,15 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
         if ((st = dalloc(c, &p, N ? N : 1))) return st;
         t.req_state = (uint8_t*)p;
-        if ((st = dalloc(c, &p, stepwise_extra_bytes(R)))) return st;
+        if ((st = dalloc(c, &p, stepwise_extra_bytes(R, N)))) return st;
         c->sw = stepwise_bind(p, R);
     }
 
-    TCM_CUDA(c, cudaMemsetAsync(t.cal, 0xFF, (size_t)R * kCalSlots * 4, s));
-    TCM_CUDA(c, cudaMemsetAsync(t.occ, 0, (size_t)R * kCalWords * 4, s));
-    TCM_CUDA(c, cudaMemsetAsync(t.first_token, 0, 8 * N, s));
-    TCM_CUDA(c, cudaMemsetAsync(t.done, 0, 8 * N, s));
-    TCM_CUDA(c, cudaMemsetAsync(t.admit_seq, 0xFF, 4 * N, s));
-    if (t.req_state) TCM_CUDA(c, cudaMemsetAsync(t.req_state, 0, N ? N : 1, s));
-    launch_init(t, s);
-    c->launches++;
+    c->t = t;
+    {
+        tcm_status rs = reset_state(c);
+        if (rs != TCM_OK) return rs;
+    }
 
     // validate on the device (R18)
     uint32_t hv[2] = {0, 0xFFFFFFFFu};
@@ -293,10 +312,15 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     if (hv[0] != ST_OK)
         return fail(c, TCM_E_ARG, "replica %u: malformed trace or params (footprint/out/modality/"
                     "arrival order/policy/budget/kv/alpha)", hv[1]);
-    c->t = t;
     c->loaded = true;
     c->err.clear();
     return TCM_OK;
+}
+
+tcm_status tcm_reset(tcm_ctx* c) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_reset before tcm_load_trace");
+    return reset_state(c);
 }
 
 tcm_status tcm_step(tcm_ctx* c, uint32_t max_iterations, uint32_t* active_replicas) {

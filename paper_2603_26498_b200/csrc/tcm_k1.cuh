@@ -31,13 +31,24 @@ constexpr double kLn2d16Hi = 0x1.62e42fee00000p-5;
 constexpr double kLn2d16Lo = 0x1.a39ef35793c76p-37;
 constexpr double kEps = 1e-12;
 
+// Table access: the fused engine reads the __constant__ copies (few keys per decision); the
+// stepwise engine stages them in shared memory (divergent j across a warp would serialise
+// constant-cache reads).
+struct K1Tables {
+    const double* lnR;
+    const double* lnT;
+    const double* expT;
+};
+
+__device__ __forceinline__ K1Tables k1_const_tables() { return K1Tables{kLnR, kLnT, kExpT}; }
+
 // LN(v), v a positive normal double: steps LN.1-LN.6.
-__device__ __forceinline__ double k1_ln(double v) {
+__device__ __forceinline__ double k1_ln(double v, const K1Tables& tb = k1_const_tables()) {
     const uint64_t b = (uint64_t)__double_as_longlong(v);
     const int e = (int)((b >> 52) & 0x7FF) - 1023;
     const int j = (int)((b >> 48) & 0xF);
     const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
-    const double u = __fma_rn(m, kLnR[j], -1.0);
+    const double u = __fma_rn(m, tb.lnR[j], -1.0);
     double q = 0x1.c71c71c71c71cp-4;                 // c9
     q = __fma_rn(q, u, -0x1p-3);                     // c8
     q = __fma_rn(q, u, 0x1.2492492492492p-3);        // c7
@@ -48,12 +59,12 @@ __device__ __forceinline__ double k1_ln(double v) {
     q = __fma_rn(q, u, -0x1p-1);                     // c2
     q = __fma_rn(q, u, 0x1p+0);                      // c1
     const double lnm = __dmul_rn(q, u);
-    const double t = __dadd_rn(kLnT[j], lnm);
+    const double t = __dadd_rn(tb.lnT[j], lnm);
     return __fma_rn((double)e, kLN2, t);
 }
 
 // EXP(y): steps EXP.1-EXP.7.
-__device__ __forceinline__ double k1_exp(double y) {
+__device__ __forceinline__ double k1_exp(double y, const K1Tables& tb = k1_const_tables()) {
     if (y < -745.0) return 0.0;
     if (y > 700.0) return __longlong_as_double(0x7FF0000000000000ll);
     const double kf = rint(__dmul_rn(y, kInvLn2x16));
@@ -69,7 +80,7 @@ __device__ __forceinline__ double k1_exp(double y) {
     const long long k = (long long)kf;
     const long long j = k & 15;
     const long long n = (k - j) / 16;
-    const double s = __dmul_rn(kExpT[j], p);
+    const double s = __dmul_rn(tb.expT[j], p);
     if (n < -1021) return 0.0;
     const double res = __dmul_rn(s, __longlong_as_double((long long)((unsigned long long)(n + 1023) << 52)));
     if (res < 0x1p-1022) return 0.0;
@@ -99,18 +110,20 @@ __device__ __forceinline__ K1Class k1_class(double S, double k, double p, double
     return kc;
 }
 
-__device__ __forceinline__ double k1_priority(const K1Class& kc, uint64_t w) {
+__device__ __forceinline__ double k1_priority(const K1Class& kc, uint64_t w,
+                                              const K1Tables& tb = k1_const_tables()) {
     if (w == 0 || kc.zero) return kc.S;
-    const double L = k1_ln(__ull2double_rn(w));
+    const double L = k1_ln(__ull2double_rn(w), tb);
     const double y = __fma_rn(kc.p, L, kc.C);
-    const double x = k1_exp(y);
-    const double e = k1_exp(-x);
+    const double x = k1_exp(y, tb);
+    const double e = k1_exp(-x, tb);
     return __dadd_rn(kc.S, __dsub_rn(1.0, e));
 }
 
 // Key: bit pattern of max(P, 1e-12), compared as unsigned, larger first.
-__device__ __forceinline__ uint64_t k1_key(const K1Class& kc, uint64_t w) {
-    double P = k1_priority(kc, w);
+__device__ __forceinline__ uint64_t k1_key(const K1Class& kc, uint64_t w,
+                                           const K1Tables& tb = k1_const_tables()) {
+    double P = k1_priority(kc, w, tb);
     P = P < kEps ? kEps : P;
     return (uint64_t)__double_as_longlong(P);
 }

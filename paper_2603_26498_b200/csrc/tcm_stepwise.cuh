@@ -10,7 +10,8 @@ struct StepwiseWorkspace {
 };
 
 size_t stepwise_workspace_bytes(uint32_t R, uint64_t N);
-size_t stepwise_extra_bytes(uint32_t R);
+size_t stepwise_extra_bytes(uint32_t R, uint64_t N);   // rem[N] + pad
+void stepwise_init(const TraceDev& t, cudaStream_t s);
 StepwiseWorkspace stepwise_bind(void* p, uint32_t R);
 // Runs up to max_iters engine iterations of every active replica; counts launches.
 tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWorkspace& w,

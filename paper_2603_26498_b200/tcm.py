@@ -25,7 +25,7 @@ MEM_DEVICE, MEM_HOST = 0, 1
 HIST_BINS, GROUPS, NCNT = 496, 4, 6
 INF32 = 0xFFFFFFFF
 
-EXPORTS = ("tcm_create", "tcm_load_trace", "tcm_step", "tcm_run", "tcm_stats", "tcm_destroy",
+EXPORTS = ("tcm_create", "tcm_load_trace", "tcm_reset", "tcm_step", "tcm_run", "tcm_stats", "tcm_destroy",
            "tcm_last_error", "tcm_workspace_bytes", "tcm_generate_trace", "tcm_k1_eval",
            "tcm_k1_audit")
 
@@ -90,6 +90,8 @@ def lib():
         L.tcm_create.argtypes = [ctypes.POINTER(tcm_config), vp, ctypes.POINTER(vp)]
         L.tcm_load_trace.restype = st
         L.tcm_load_trace.argtypes = [vp, ctypes.POINTER(tcm_trace_view), ctypes.POINTER(tcm_results_view)]
+        L.tcm_reset.restype = st
+        L.tcm_reset.argtypes = [vp]
         L.tcm_step.restype = st
         L.tcm_step.argtypes = [vp, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]
         L.tcm_run.restype = st
@@ -176,6 +178,10 @@ def tcm_load_trace(ctx, trace: dict, results: dict | None, mem=MEM_DEVICE):
         rv.first_token_us = _ptr(results.get("first_token_us"))
         rv.done_us = _ptr(results.get("done_us"))
     _check(lib().tcm_load_trace(ctx, ctypes.byref(tv), ctypes.byref(rv)), ctx)
+
+
+def tcm_reset(ctx):
+    _check(lib().tcm_reset(ctx), ctx)
 
 
 def tcm_step(ctx, max_iterations: int) -> int:
@@ -289,6 +295,9 @@ class Simulation:
 
     def run(self):
         tcm_run(self.ctx)
+
+    def reset(self):
+        tcm_reset(self.ctx)
 
     def step(self, max_iterations: int) -> int:
         return tcm_step(self.ctx, max_iterations)

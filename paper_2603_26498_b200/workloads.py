@@ -1,0 +1,121 @@
+"""Sweep grids of BASELINE.json's configs and the replica-sharding layer.
+
+A replica = one engine (trace x load x policy parameters).  Replicas never interact
+("many engines may run concurrently on independent inputs"), so a sweep
+shards across GPUs with no data-path collective: global replica g goes to rank g mod G
+(cyclic over sweep cells for load balance); only the int64 a6 histograms
+and counters are all-reduced (NCCL), which is bit-exact for any G.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import tcm
+
+try:  # the generator is the shared seeded-input module (repo root)
+    import tracegen as T
+except ImportError:  # pragma: no cover - repo root not on sys.path
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import tracegen as T
+
+
+@dataclass
+class Sweep:
+    name: str
+    gen: np.ndarray          # tracegen.TG_REPLICA_DTYPE [R]
+    params: np.ndarray       # tcm.PARAMS_DTYPE [R]
+    n_cells: int
+    cells: list              # human-readable description of each cell
+
+    @property
+    def n_replicas(self) -> int:
+        return len(self.gen)
+
+    @property
+    def n_requests(self) -> int:
+        return int(self.gen["n_requests"].sum())
+
+
+def _grid(name, cells, replicas_per_cell, n_requests, seed, replica_ids):
+    """cells: list of dicts(rate, mix, kv, policy, alpha, budget). Global replica g belongs to
+    cell g % n_cells (cyclic) and seed index g // n_cells."""
+    nc = len(cells)
+    R = len(replica_ids)
+    gen = np.zeros(R, dtype=T.TG_REPLICA_DTYPE)
+    params = tcm.make_params(R)
+    for j, g in enumerate(replica_ids):
+        c = cells[g % nc]
+        gen[j] = T.make_replica(seed, int(g), n_requests, c["rate"], c["mix"], c["kv"])
+        params[j]["policy"] = c["policy"]
+        params[j]["kv_capacity"] = c["kv"]
+        params[j]["aging_alpha"] = c["alpha"]
+        params[j]["chunk_budget"] = c["budget"]
+        params[j]["cell_id"] = g % nc
+    return Sweep(name, gen, params, nc, cells)
+
+
+ALPHAS = [0.0] + [2.0 ** e for e in range(-7, 8)]          # R14: {0} U {2^-7 .. 2^7}
+
+
+def c1(policy=tcm.POLICY_TCM, seed=1):
+    """1 replica x 1,000 requests, 70/25/5, 2 req/s, KV 131072, B 2048."""
+    cells = [dict(rate=2.0, mix=(0.70, 0.25, 0.05), kv=131072, policy=policy, alpha=1.0, budget=2048)]
+    return _grid("C1", cells, 1, 1000, seed, [0])
+
+
+def c3(rank=0, world=1, replicas=4096, n_requests=10_000, seed=2026):
+    """4,096 replicas x 10k: lambda in {0.25..4.0} (16) x alpha (16) x 16 seeds, 70/25/5, TCM."""
+    cells = [dict(rate=0.25 * (i + 1), mix=(0.70, 0.25, 0.05), kv=131072, policy=tcm.POLICY_TCM,
+                  alpha=a, budget=2048) for i in range(16) for a in ALPHAS]
+    return _grid("C3", cells, replicas // len(cells), n_requests, seed, range(rank, replicas, world))
+
+
+def c4_cells():
+    return [dict(rate=lam, mix=(0.50, 0.20, 0.30), kv=kv, policy=pol, alpha=1.0, budget=2048)
+            for pol in (tcm.POLICY_FCFS, tcm.POLICY_TCM) for lam in (0.5, 1.0, 2.0, 4.0)
+            for kv in (131072, 65536, 32768, 16384)]
+
+
+def c4(rank=0, world=1, replicas_per_gpu=65536, n_requests=10_000, seed=4044):
+    """Memory-pressure sweep (video-heavy 50/20/30, tight KV): KV {128k,64k,32k,16k} x lambda
+    {0.5,1,2,4} x {FCFS,TCM} x seeds.  Weak scaling: every rank simulates replicas_per_gpu
+    replicas; global replica ids rank, rank+G, ... (cyclic over the 32 cells)."""
+    total = replicas_per_gpu * world
+    return _grid("C4", c4_cells(), total // 32, n_requests, seed, range(rank, total, world))
+
+
+def c5_cells():
+    mixes = [T.MIXES[k] for k in ("TO", "ML", "MH", "70/25/5", "50/20/30", "80/20/0", "80/0/20", "40/40/20")]
+    budgets = [256 << i for i in range(8)]                      # 256 .. 32768
+    return [dict(rate=0.25 * (i + 1), mix=mx, kv=131072, policy=tcm.POLICY_TCM, alpha=a, budget=b)
+            for i in range(16) for mx in mixes for a in ALPHAS for b in budgets]
+
+
+def c5(rank=0, world=8, replicas=1 << 20, n_requests=10_000, seed=5055):
+    """1M replicas x 10k: 16 lambda x 8 mixes x 16 alpha x 8 budgets (16,384 cells) x 64 seeds."""
+    return _grid("C5", c5_cells(), replicas // 16384, n_requests, seed, range(rank, replicas, world))
+
+
+def c2prime(replicas=65536, pending=1024, seed=2222):
+    """C2': many replicas x ~1k pending requests, for the per-step kernels' HBM
+    roofline.  Request 0 of each replica carries 60 s of inline encode time, so when the second
+    iteration starts every other request (arrivals spread over ~60 s) is pending with a
+    distinct waiting time."""
+    rate = pending / 60.0
+    cells = [dict(rate=rate, mix=(0.70, 0.25, 0.05), kv=131072, policy=tcm.POLICY_TCM, alpha=1.0, budget=2048)]
+    sw = _grid("C2'", cells, replicas, pending, seed, range(replicas))
+    return sw
+
+
+def stage_c2prime(trace_np):
+    """Make request 0 of every replica a 60 s-inline image so the clock jumps past all arrivals."""
+    off = trace_np.offset
+    first = off[:-1].astype(np.int64)
+    trace_np.inline_us[first] = 60_000_000
+    trace_np.modality[first] = 1
+    trace_np.footprint[first] = 800
+    return trace_np
