@@ -117,18 +117,21 @@ def _oracle_job(job):
     return dt, n, r.counters["decisions"]
 
 
-def oracle_sample(sweep, budget_s=20.0, n_trunc=1000, max_jobs=None):
-    """Time the oracle (as it stands) on a bounded sample: every (R/64)-th replica of the sweep
-    truncated to its first n_trunc requests, one replica per process on the host cores."""
+def oracle_sample(sweep, n_trunc=1000, per_cell=1):
+    """Time the oracle (as it stands) on a bounded sample of the sweep: `per_cell` replicas of
+    every cell, truncated to their first n_trunc requests, one replica per process on the host
+    cores."""
     import multiprocessing as mp
     R = sweep.n_replicas
-    step = max(1, R // 64)
-    idx = list(range(0, R, step))[: (max_jobs or 64)]
+    cells = sweep.params["cell_id"]
+    idx = []
+    for c in range(sweep.n_cells):
+        idx.extend(np.nonzero(cells == c)[0][:per_cell].tolist())
     jobs = [(sweep.gen[i], int(sweep.params[i]["policy"]), int(sweep.params[i]["kv_capacity"]),
              float(sweep.params[i]["aging_alpha"]), int(sweep.params[i]["chunk_budget"]), n_trunc) for i in idx]
     cores = min(len(jobs), os.cpu_count() or 1)
     t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(cores) as pool:
+    with mp.get_context("spawn").Pool(cores) as pool:     # never fork a CUDA process
         res = pool.map(_oracle_job, jobs, chunksize=1)
     wall = time.perf_counter() - t0
     nreq = sum(r[1] for r in res)
@@ -144,26 +147,26 @@ def run_reference(args, rank, world):
     from paper_2603_26498_b200 import workloads as W
     sw = W.c4(0, 1, replicas_per_gpu=args.replicas, n_requests=args.requests)
     for _ in range(args.warmup):
-        oracle_sample(sw, n_trunc=args.ref_requests, max_jobs=16)
+        oracle_sample(sw, n_trunc=args.ref_requests)
     tot_req = tot_dec = 0
     tot_wall = 0.0
     cores = 0
     for _ in range(args.steps):
-        s = oracle_sample(sw, n_trunc=args.ref_requests, max_jobs=16)
+        s = oracle_sample(sw, n_trunc=args.ref_requests)
         tot_req += s["requests"]
         tot_dec += s["decisions"]
         tot_wall += s["wall_s"]
         cores = s["cores"]
     v = tot_req / tot_wall
-    sample = (f"16 replicas of C4 (every {max(1, sw.n_replicas // 64)}th), first {args.ref_requests} requests each, "
-              f"one oracle process per replica")
+    sample = (f"one replica of each of the 32 C4 cells, first {args.ref_requests} requests each, "
+              f"one oracle process per replica on {cores} host cores")
     line = {
         "impl": "reference", "metric": "simulated requests/sec (C4 memory-pressure sweep)", "value": v,
         "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
         "decisions_per_s": tot_dec / tot_wall,
-        "config": {"workload": "C4 memory-pressure sweep (bounded oracle sample)", "replicas": 16,
+        "config": {"workload": "C4 memory-pressure sweep (bounded oracle sample)", "replicas": 32,
                    "requests_per_replica": args.ref_requests},
         "cpu_baseline": {"value": v, "unit": "requests/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -187,6 +190,7 @@ def run_tcm(args, rank, world, local):
 
     sw = W.c4(rank, world, replicas_per_gpu=args.replicas, n_requests=args.requests)
     R, N = sw.n_replicas, sw.n_requests
+    log(f"rank {rank}: C4 shard {R} replicas, {N} requests; generating on device")
     with torch.cuda.stream(stream):
         trace = tcm.generate_device(sw.gen, device=dev, stream=stream)
         trace["params"] = torch.from_numpy(sw.params.view(np.uint8)).to(dev)
@@ -208,13 +212,13 @@ def run_tcm(args, rank, world, local):
         tcm.tcm_stats(sim.ctx, hist, cnt)
         if dist is not None:
             with torch.cuda.stream(stream):
-                dist.all_reduce(hist)
-                dist.all_reduce(cnt)
+                W.allreduce_aggregate(hist, cnt)      # int64 SUM over NVLink (NCCL)
         return e0, e1
 
     for _ in range(args.warmup):
         one_step()
     stream.synchronize()
+    log("warm-up done")
     st0 = sim.stats()
     if dist is not None:
         dist.barrier()
@@ -285,20 +289,23 @@ def run_tcm(args, rank, world, local):
                  "run_ms": run_ms},
     }
 
+    log(f"timed: {ms:.1f} ms for {args.steps} steps")
     # stepwise (paper-literal) per-step kernel on C2': its own HBM roofline
     if not args.skip_step and rank == 0:
         out["roofline_step"] = bench_stepwise(args, dev, stream)
 
     # end-to-end through the C ABI with HOST buffers (H2D + run + D2H inside the timed region)
+    log("stepwise done")
     if not args.skip_e2e:
         out["e2e"] = bench_e2e(args, sw, trace, dev, stream, dist, world)
+    log("e2e done")
 
     if rank == 0 and not args.skip_cpu:
-        s = oracle_sample(sw, n_trunc=args.ref_requests, max_jobs=16)
+        s = oracle_sample(sw, n_trunc=args.ref_requests)
         out["cpu_baseline"] = {"value": s["requests"] / s["wall_s"], "unit": "requests/s", "cores": s["cores"],
                                "kind": "oracle",
                                "decisions_per_s": s["decisions"] / s["wall_s"],
-                               "sample": f"{s['replicas']} C4 replicas (every {max(1, R // 64)}th), first "
+                               "sample": f"{s['replicas']} C4 replicas (one per cell), first "
                                          f"{s['n_trunc']} requests each, one oracle process per replica, "
                                          f"{s['wall_s']:.1f} s wall"}
     sim.close()
@@ -403,7 +410,13 @@ def bench_e2e(args, sw, trace, dev, stream, dist, world):
             "note": "HOST pinned buffers through tcm_load_trace/tcm_run/tcm_stats; host wall clock, max over ranks"}
 
 
+def log(*a):
+    print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
+
+
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("BENCH_HANG_DUMP_S", "1500")), exit=False)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -411,7 +424,7 @@ def main():
     ap.add_argument("--impl", choices=["tcm", "reference"], default="tcm")
     ap.add_argument("--replicas", type=int, default=65536, help="C4 replicas per GPU")
     ap.add_argument("--requests", type=int, default=10_000)
-    ap.add_argument("--ref-requests", type=int, default=1000, help="oracle sample: requests per replica")
+    ap.add_argument("--ref-requests", type=int, default=2000, help="oracle sample: requests per replica")
     ap.add_argument("--step-replicas", type=int, default=65536)
     ap.add_argument("--step-pending", type=int, default=1024)
     ap.add_argument("--step-iters", type=int, default=4)

@@ -291,6 +291,9 @@ class Simulation:
         self.ctx = tcm_create(self.cfg, self.stream)
 
     def load(self, trace: dict, results: dict | None = None, mem=MEM_DEVICE):
+        # the library borrows every buffer until destroy / the next load (include/tcm.h):
+        # keep them alive here so torch's allocator cannot recycle them underneath it
+        self._borrowed = (trace, results)
         tcm_load_trace(self.ctx, trace, results, mem)
 
     def run(self):
@@ -317,6 +320,7 @@ class Simulation:
         if self.ctx:
             tcm_destroy(self.ctx)
             self.ctx = None
+        self._borrowed = None
 
     def __del__(self):
         try:

@@ -2,8 +2,9 @@
 
 A replica = one engine (trace x load x policy parameters).  Replicas never interact
 ("many engines may run concurrently on independent inputs"), so a sweep
-shards across GPUs with no data-path collective: global replica g goes to rank g mod G
-(cyclic over sweep cells for load balance); only the int64 a6 histograms
+shards across GPUs with no data-path collective: global replica g = seed*n_cells + cell goes to
+rank seed mod G
+(seed rows dealt cyclically so every rank holds every cell); only the int64 a6 histograms
 and counters are all-reduced (NCCL), which is bit-exact for any G.
 """
 from __future__ import annotations
@@ -40,9 +41,17 @@ class Sweep:
         return int(self.gen["n_requests"].sum())
 
 
+def rank_ids(n_cells: int, seeds_total: int, rank: int, world: int) -> list:
+    """Global replica ids g = seed * n_cells + cell owned by `rank`: seed rows are dealt
+    cyclically (seed % world == rank), so every rank holds every cell in equal measure (load
+    balance: cells differ ~100x in cost); ids are ordered cell-major so a warp's 32 replicas
+    share one cell's parameters (SIMT coherence)."""
+    return [s * n_cells + c for c in range(n_cells) for s in range(rank, seeds_total, world)]
+
+
 def _grid(name, cells, replicas_per_cell, n_requests, seed, replica_ids):
     """cells: list of dicts(rate, mix, kv, policy, alpha, budget). Global replica g belongs to
-    cell g % n_cells (cyclic) and seed index g // n_cells."""
+    cell g % n_cells and seed row g // n_cells."""
     nc = len(cells)
     R = len(replica_ids)
     gen = np.zeros(R, dtype=T.TG_REPLICA_DTYPE)
@@ -71,7 +80,8 @@ def c3(rank=0, world=1, replicas=4096, n_requests=10_000, seed=2026):
     """4,096 replicas x 10k: lambda in {0.25..4.0} (16) x alpha (16) x 16 seeds, 70/25/5, TCM."""
     cells = [dict(rate=0.25 * (i + 1), mix=(0.70, 0.25, 0.05), kv=131072, policy=tcm.POLICY_TCM,
                   alpha=a, budget=2048) for i in range(16) for a in ALPHAS]
-    return _grid("C3", cells, replicas // len(cells), n_requests, seed, range(rank, replicas, world))
+    nc = len(cells)
+    return _grid("C3", cells, replicas // nc, n_requests, seed, rank_ids(nc, replicas // nc, rank, world))
 
 
 def c4_cells():
@@ -84,8 +94,9 @@ def c4(rank=0, world=1, replicas_per_gpu=65536, n_requests=10_000, seed=4044):
     """Memory-pressure sweep (video-heavy 50/20/30, tight KV): KV {128k,64k,32k,16k} x lambda
     {0.5,1,2,4} x {FCFS,TCM} x seeds.  Weak scaling: every rank simulates replicas_per_gpu
     replicas; global replica ids rank, rank+G, ... (cyclic over the 32 cells)."""
-    total = replicas_per_gpu * world
-    return _grid("C4", c4_cells(), total // 32, n_requests, seed, range(rank, total, world))
+    cells = c4_cells()
+    seeds_total = replicas_per_gpu * world // len(cells)
+    return _grid("C4", cells, seeds_total, n_requests, seed, rank_ids(len(cells), seeds_total, rank, world))
 
 
 def c5_cells():
@@ -97,7 +108,9 @@ def c5_cells():
 
 def c5(rank=0, world=8, replicas=1 << 20, n_requests=10_000, seed=5055):
     """1M replicas x 10k: 16 lambda x 8 mixes x 16 alpha x 8 budgets (16,384 cells) x 64 seeds."""
-    return _grid("C5", c5_cells(), replicas // 16384, n_requests, seed, range(rank, replicas, world))
+    cells = c5_cells()
+    nc = len(cells)
+    return _grid("C5", cells, replicas // nc, n_requests, seed, rank_ids(nc, replicas // nc, rank, world))
 
 
 def c2prime(replicas=65536, pending=1024, seed=2222):
@@ -119,3 +132,13 @@ def stage_c2prime(trace_np):
     trace_np.modality[first] = 1
     trace_np.footprint[first] = 800
     return trace_np
+
+
+def allreduce_aggregate(hist, cnt):
+    """Sum the int64 a6 histograms / counters over all ranks (NCCL on GPUs, gloo on CPU).
+    Integer sums are order-independent, so the result is bit-identical for any world size."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(hist)
+        dist.all_reduce(cnt)
+    return hist, cnt
