@@ -94,15 +94,22 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
 #pragma unroll
     for (int c = 0; c < 3; ++c) kc[c] = k1_class(m.S[c], m.k[c], m.p[c], prm.aging_alpha);
 
-    // Cached arrival / footprint of each queue head.
-    uint64_t harr[3];
-    uint32_t hf[3];
+    // Register caches: each class queue's head (arrival, footprint) and its successor
+    // (id, arrival, footprint) so that advancing a queue never waits on memory; the next
+    // decode-calendar event, so that iterations without a finish never touch the calendar.
+    uint64_t harr[3], sarr[3];
+    uint32_t hf[3], sid[3], sf[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        harr[c] = st.head[c] != NIL ? arr[st.head[c]] : 0;
-        hf[c] = st.head[c] != NIL ? fp[st.head[c]] : 0;
+        const uint32_t h = st.head[c];
+        harr[c] = h != NIL ? arr[h] : 0;
+        hf[c] = h != NIL ? fp[h] : 0;
+        sid[c] = (h != NIL && h != st.tail[c]) ? link[h] : NIL;
+        sarr[c] = sid[c] != NIL ? arr[sid[c]] : 0;
+        sf[c] = sid[c] != NIL ? fp[sid[c]] : 0;
     }
     uint64_t next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
+    uint64_t next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
     uint32_t budget = max_iters;
 
     for (;;) {
@@ -120,8 +127,14 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
                         st.flags &= ~(1u << c);
                         harr[c] = next_arr;
                         hf[c] = f;
+                        sid[c] = NIL;
                     } else {
                         link[st.tail[c]] = i;
+                        if (sid[c] == NIL) {               // head was alone: i is its successor
+                            sid[c] = i;
+                            sarr[c] = next_arr;
+                            sf[c] = f;
+                        }
                     }
                     st.tail[c] = i;
                 }
@@ -143,7 +156,7 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
             }
             if (budget == 0) break;
             // ---- Lemma L3: decode-only iterations until the next finish or arrival
-            const uint64_t F = cal_next(cal, st.iter);
+            const uint64_t F = next_fin;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = F - st.iter;
             if (next_arr != ~0ull) {
@@ -155,7 +168,10 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
             st.iter += j;
             st.ff_iters += j;
             budget -= (uint32_t)j;
-            if (st.iter == F) cal_process(cal, link, st.iter, st.clock, fp, done, st);
+            if (st.iter == F) {
+                cal_process(cal, link, st.iter, st.clock, fp, done, st);
+                next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
+            }
             continue;
         }
         if (budget == 0) break;
@@ -164,8 +180,8 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
         uint32_t left = B > st.n_dec ? B - st.n_dec : 0;   // R8
         uint64_t tok = 0, inl_sum = 0;
         bool blocked = false;                               // R6
-        uint32_t cur[3], crem[3], cf[3];
-        uint64_t carr[3], key[3];
+        uint32_t cur[3], crem[3], cf[3], csid[3], csf[3];
+        uint64_t carr[3], key[3], csarr[3];
         bool cres[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -173,6 +189,9 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
             crem[c] = st.rem[c];
             carr[c] = harr[c];
             cf[c] = hf[c];
+            csid[c] = sid[c];
+            csarr[c] = sarr[c];
+            csf[c] = sf[c];
             cres[c] = (st.flags >> c) & 1u;
             key[c] = (prio && cur[c] != NIL) ? k1_key(kc[c], st.clock - carr[c]) : 0;
         }
@@ -218,14 +237,18 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
                         if (crem[c] == 0) {                 // prefill complete: next in FIFO
                             if (i == st.tail[c]) {
                                 cur[c] = NIL;
+                                csid[c] = NIL;
                             } else {
-                                const uint32_t ni = link[i];
+                                const uint32_t ni = csid[c];   // prefetched successor
                                 cur[c] = ni;
-                                carr[c] = arr[ni];
-                                cf[c] = fp[ni];
+                                carr[c] = csarr[c];
+                                cf[c] = csf[c];
                                 crem[c] = cf[c];
                                 cres[c] = false;
                                 if (prio) key[c] = k1_key(kc[c], st.clock - carr[c]);
+                                csid[c] = ni != st.tail[c] ? link[ni] : NIL;
+                                csarr[c] = csid[c] != NIL ? arr[csid[c]] : 0;
+                                csf[c] = csid[c] != NIL ? fp[csid[c]] : 0;
                             }
                         }
                     }
@@ -245,7 +268,11 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
         st.sum_pending += st.n_pend;
         st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
         budget--;
-        cal_process(cal, link, st.iter, st.clock, fp, done, st);
+        bool recompute_fin = false;
+        if (st.iter == next_fin) {
+            cal_process(cal, link, st.iter, st.clock, fp, done, st);
+            recompute_fin = true;
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             uint32_t i = st.head[c];
@@ -259,8 +286,10 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
                     st.kv_free += fp[i];
                     st.done_count++;
                 } else {
-                    cal_insert(cal, link, (uint32_t)((st.iter + o - 1) & (kCalSlots - 1)), i);
+                    const uint64_t fin = st.iter + o - 1;
+                    cal_insert(cal, link, (uint32_t)(fin & (kCalSlots - 1)), i);
                     st.n_dec++;
+                    next_fin = fin < next_fin ? fin : next_fin;
                 }
                 i = ni;
             }
@@ -270,7 +299,11 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
             st.flags = cres[c] ? (st.flags | (1u << c)) : (st.flags & ~(1u << c));
             harr[c] = carr[c];
             hf[c] = cf[c];
+            sid[c] = csid[c];
+            sarr[c] = csarr[c];
+            sf[c] = csf[c];
         }
+        if (recompute_fin) next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
     }
 
     t.state[r] = st;

@@ -1,20 +1,23 @@
 // tcm_stepwise.cu -- TCM_ENGINE_STEPWISE: the paper-literal per-iteration scheduling step.
 //
-// Every engine iteration, for every active replica, one CTA:
-//   a1  ingests arrivals <= clock (warp-parallel ballot over the sorted arrivals) and
-//       classifies them (R13) into the per-request state byte;
+// Every engine iteration, for every active replica, one GROUP of G warps (G = 1: a warp per
+// replica, for sweeps of many replicas; G = 8: a CTA per replica, for a few huge queues):
+//   a1  ingests arrivals <= clock (ballots over 128 sorted arrivals per round) and classifies
+//       them (R13) into the per-request state byte;
 //   a2  re-keys EVERY pending request of the replica's window [lo, nxt) with K1
 //       ("At each scheduling iteration ... evaluates the state of all queues and dynamically
-//       adjusts priorities") -- a coalesced, vectorised SoA stream of
-//       arrival (8 B) + state (1 B) per request; the key is never written to memory;
-//   a3  selects the top-32 candidates by (key desc, id asc) with per-warp register lists
-//       merged by warp-shuffle bitonic networks (ballot skips batches that cannot enter);
-//   a4  admits by warp-shuffle prefix scans of footprints against free KV and of chunk
-//       tokens against the budget (R5-R8); if the scan has not terminated after 32
-//       candidates it re-streams for the next 32 (threshold = last selected);
-//   a5  advances the clock, stamps first tokens and runs the decode calendar (identical
-//       integer arithmetic to the fused engine), with the decode-only fast-forward.
-// Nothing here relies on Lemma L1, so any per-request key function fits this path.
+//       adjusts priorities"): a coalesced, vectorised, software-pipelined
+//       SoA stream of arrival (8 B) + state (1 B) per request; the key is never stored;
+//   a3  selects the top-32 candidates by (key desc, id asc): per-warp register lists updated
+//       by warp-shuffle bitonic networks (a ballot skips batches that cannot enter), merged
+//       across the group's warps through shared memory;
+//   a4  admits by warp-shuffle prefix scans of footprints against free KV and of chunk tokens
+//       against the budget (R5-R8); if the scan has not terminated after 32 candidates it
+//       re-streams for the next 32 (threshold = last selected); partials ranked below a KV
+//       block keep their chunks (R6);
+//   a5  advances the clock, stamps first tokens and runs the decode calendar (same integer
+//       arithmetic as the fused engine), with the decode-only fast-forward (Lemma L3).
+// Nothing here relies on Lemma L1 (class-FIFO order), so any per-request key fits this path.
 #include "tcm_k1.cuh"
 #include "tcm_stepwise.cuh"
 
@@ -23,43 +26,29 @@ namespace tcm {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr int kTop = 32;
 constexpr int kMaxPart = 32;
-constexpr int kMaxDone = 1024;
 constexpr uint32_t ST_PARTIAL_OVERFLOW = 4;
 
 // request-state byte
 constexpr uint8_t RS_CLS = 3, RS_PEND = 4, RS_RES = 8, RS_FT = 16;
 
-struct Key {
-    uint64_t k;
-    uint32_t i;
-};
-
 __device__ __forceinline__ bool before(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
     return ka > kb || (ka == kb && ia < ib);
 }
 
-__device__ __forceinline__ void shfl_key(uint64_t& k, uint32_t& i, int lane_src_xor) {
-    k = __shfl_xor_sync(0xFFFFFFFFu, k, lane_src_xor);
-    i = __shfl_xor_sync(0xFFFFFFFFu, i, lane_src_xor);
-}
-
-// Bitonic sort of one element per lane, descending in (key, -id) across lanes 0..31.
+// Bitonic sort of one (key, id) per lane, descending across lanes 0..31.
 __device__ __forceinline__ void warp_sort_desc(uint64_t& k, uint32_t& i, int lane) {
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
         for (int j = size >> 1; j > 0; j >>= 1) {
-            uint64_t pk = k;
-            uint32_t pi = i;
-            shfl_key(pk, pi, j);
+            const uint64_t pk = __shfl_xor_sync(0xFFFFFFFFu, k, j);
+            const uint32_t pi = __shfl_xor_sync(0xFFFFFFFFu, i, j);
             const bool desc = (lane & size) == 0 || size == 32;
             const bool lower = (lane & j) == 0;
-            const bool want_better = (lower == desc);
-            const bool p_better = before(pk, pi, k, i);
-            if (want_better ? p_better : before(k, i, pk, pi)) {
+            if ((lower == desc) ? before(pk, pi, k, i) : before(k, i, pk, pi)) {
                 k = pk;
                 i = pi;
             }
@@ -67,23 +56,8 @@ __device__ __forceinline__ void warp_sort_desc(uint64_t& k, uint32_t& i, int lan
     }
 }
 
-// After element-wise max of a descending list and a reversed descending list, the 32
-// values form a bitonic sequence holding the top 32; clean it into descending order.
-__device__ __forceinline__ void warp_bitonic_clean_desc(uint64_t& k, uint32_t& i, int lane) {
-#pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
-        uint64_t pk = k;
-        uint32_t pi = i;
-        shfl_key(pk, pi, j);
-        const bool lower = (lane & j) == 0;
-        if (lower ? before(pk, pi, k, i) : before(k, i, pk, pi)) {
-            k = pk;
-            i = pi;
-        }
-    }
-}
-
-// Merge a descending batch (bk, bi) into the descending list (lk, li): keeps the top 32.
+// Merge a descending batch into a descending list, keeping the top 32: element-wise max with
+// the reversed batch gives a bitonic sequence holding the top 32; clean it.
 __device__ __forceinline__ void warp_merge(uint64_t& lk, uint32_t& li, uint64_t bk, uint32_t bi, int lane) {
     const uint64_t rk = __shfl_sync(0xFFFFFFFFu, bk, 31 - lane);
     const uint32_t ri = __shfl_sync(0xFFFFFFFFu, bi, 31 - lane);
@@ -91,7 +65,16 @@ __device__ __forceinline__ void warp_merge(uint64_t& lk, uint32_t& li, uint64_t 
         lk = rk;
         li = ri;
     }
-    warp_bitonic_clean_desc(lk, li, lane);
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint64_t pk = __shfl_xor_sync(0xFFFFFFFFu, lk, j);
+        const uint32_t pi = __shfl_xor_sync(0xFFFFFFFFu, li, j);
+        const bool lower = (lane & j) == 0;
+        if (lower ? before(pk, pi, lk, li) : before(lk, li, pk, pi)) {
+            lk = pk;
+            li = pi;
+        }
+    }
 }
 
 __device__ __forceinline__ uint64_t warp_incl_scan64(uint64_t v, int lane) {
@@ -146,27 +129,34 @@ __device__ __forceinline__ uint64_t cal_next(const Cal& c, uint64_t iter) {
     return iter + 1 + (uint64_t)(dist + (uint32_t)(__ffs(w) - 1));
 }
 
-struct Smem {
-    double lnR[16], lnT[16], expT[16];
-    uint64_t wkey[kWarps][kTop];
-    uint32_t wid[kWarps][kTop];
+// Per-group shared state.
+template <int G>
+struct GroupSmem {
+    static constexpr int kMaxDone = G == 1 ? 128 : 1024;
+    uint64_t wkey[G][kTop];
+    uint32_t wid[G][kTop];
     uint64_t partkey[kMaxPart];
     uint32_t part[kMaxPart];
     uint32_t done[kMaxDone];
     ReplicaState st;
     K1Class kc[3];
-    uint64_t thk;       // continuation threshold (exclude ranks <= (thk, thi))
+    uint64_t thk;       // continuation threshold: exclude ranks <= (thk, thi)
     uint64_t left, tok, inl;
     uint32_t thi;
     int npart, ndone, mode, pass_more, blocked, has_th;
 };
 
-}  // namespace
+template <int G>
+__device__ __forceinline__ void group_sync() {
+    if (G == 1) __syncwarp();
+    else __syncthreads();
+}
 
-// Stage the replica's state at the start of a step (warp 0): ingest, idle jumps and the
-// decode-only fast-forward.  mode: 0 nothing more this launch, 1 decision iteration.
-__device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, Smem& sm, int lane) {
-    ReplicaState st = t.state[r];                      // every lane keeps a copy
+// Prologue (warp 0 of the group): ingest, idle jumps, decode-only fast-forward.
+// mode: 0 = nothing more this launch, 1 = decision iteration.
+template <int G>
+__device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, GroupSmem<G>& sm, int lane) {
+    ReplicaState st = t.state[r];
     const uint64_t base = t.offset[r];
     const uint32_t n = (uint32_t)(t.offset[r + 1] - base);
     const uint64_t* arr = t.arrival + base;
@@ -178,19 +168,27 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
     if (!(st.flags & FLAG_FINISHED) && st.head[1] > 0) {
         const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};
         for (;;) {
-            // a1: ingest (ballot over the next 32 arrivals; arrivals are sorted)
+            // a1: ingest -- 128 sorted arrivals per round, all four loads in flight together
             for (;;) {
-                const uint32_t i = st.nxt + lane;
-                const bool in = i < n && arr[i] <= st.clock;
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, in);
-                if (in) {
-                    const int c = prio ? classify(m, mod[i], fp[i]) : 0;
-                    rs[i] = (uint8_t)(c | RS_PEND);
+                uint32_t cnt = 0;
+                bool in[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t i = st.nxt + 32 * j + lane;
+                    in[j] = i < n && arr[i] <= st.clock;
                 }
-                const uint32_t cnt = __popc(bal);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t i = st.nxt + 32 * j + lane;
+                    if (in[j]) {
+                        const int c = prio ? classify(m, mod[i], fp[i]) : 0;
+                        rs[i] = (uint8_t)(c | RS_PEND);
+                    }
+                    cnt += __popc(__ballot_sync(0xFFFFFFFFu, in[j]));
+                }
                 st.nxt += cnt;
                 st.n_pend += cnt;
-                if (cnt < 32) break;
+                if (cnt < 128) break;
             }
             if (st.n_pend > 0) {
                 mode = 1;
@@ -205,8 +203,7 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
                 st.idle_jumps++;
                 continue;
             }
-            // Lemma L3 decode-only fast-forward (same closed form as the fused engine)
-            if (lane == 0) {
+            if (lane == 0) {                             // Lemma L3 decode-only fast-forward
                 const uint64_t F = cal_next(cal, st.iter);
                 const uint64_t dt = m.c0 + m.cd * st.n_dec;
                 uint64_t j = F - st.iter;
@@ -230,27 +227,35 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
-                                                   int count_active) {
-    __shared__ Smem sm;
+}  // namespace
+
+template <int G>
+__global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
+                                                      int count_active) {
+    constexpr int kGroups = kWarpsPerBlock / G;
+    constexpr int kMaxDone = GroupSmem<G>::kMaxDone;
+    __shared__ double s_lnR[16], s_lnT[16], s_expT[16];
+    __shared__ GroupSmem<G> smg[kGroups];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int group = warp / G, wg = warp % G;       // warp index inside the group
+    GroupSmem<G>& sm = smg[group];
     if (tid < 16) {
-        sm.lnR[tid] = kLnR[tid];
-        sm.lnT[tid] = kLnT[tid];
-        sm.expT[tid] = kExpT[tid];
+        s_lnR[tid] = kLnR[tid];
+        s_lnT[tid] = kLnT[tid];
+        s_expT[tid] = kExpT[tid];
     }
     __syncthreads();
-    const K1Tables tb{sm.lnR, sm.lnT, sm.expT};
+    const K1Tables tb{s_lnR, s_lnT, s_expT};
 
-    for (uint32_t r = blockIdx.x; r < t.R; r += gridDim.x) {
-        if (warp == 0) sw_prologue(m, t, r, sm, lane);
-        __syncthreads();
+    for (uint32_t r = blockIdx.x * kGroups + group; r < t.R; r += gridDim.x * kGroups) {
+        if (wg == 0) sw_prologue<G>(m, t, r, sm, lane);
+        group_sync<G>();
         if (sm.mode == 0) {
-            if (tid == 0) {
+            if (wg == 0 && lane == 0) {
                 t.state[r] = sm.st;
                 if (count_active && !(sm.st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
             }
-            __syncthreads();
+            group_sync<G>();
             continue;
         }
 
@@ -265,41 +270,41 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
         uint32_t* rem = remv + base;
         const uint64_t clock = sm.st.clock;
         const uint32_t lo = sm.st.head[0], hi = sm.st.nxt;
-        if (tid < 3) sm.kc[tid] = k1_class(m.S[tid], m.k[tid], m.p[tid], prm.aging_alpha);
-        if (tid == 0) {
-            const uint32_t B = prm.chunk_budget;
-            sm.left = B > sm.st.n_dec ? B - sm.st.n_dec : 0;     // R8
-            sm.tok = 0;
-            sm.inl = 0;
-            sm.blocked = 0;
-            sm.has_th = 0;
-            sm.npart = 0;
-            sm.ndone = 0;
+        if (wg == 0) {
+            if (lane < 3) sm.kc[lane] = k1_class(m.S[lane], m.k[lane], m.p[lane], prm.aging_alpha);
+            if (lane == 0) {
+                const uint32_t B = prm.chunk_budget;
+                sm.left = B > sm.st.n_dec ? B - sm.st.n_dec : 0;     // R8
+                sm.tok = 0;
+                sm.inl = 0;
+                sm.blocked = 0;
+                sm.has_th = 0;
+                sm.npart = 0;
+                sm.ndone = 0;
+            }
         }
-        __syncthreads();
-        K1Class kc[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) kc[c] = sm.kc[c];
+        group_sync<G>();
+        const K1Class kc0 = sm.kc[0], kc1 = sm.kc[1], kc2 = sm.kc[2];
 
         for (int pass = 0;; ++pass) {
             const bool first_pass = pass == 0;
             const bool has_th = sm.has_th;
             const uint64_t thk = sm.thk;
             const uint32_t thi = sm.thi;
-            // ---- a2 + a3: stream the window, key, per-warp top-32
-            uint64_t lk = 0;
-            uint32_t li = NIL;
-            uint64_t kk = 0;          // current 32nd of the warp list (broadcast)
-            uint32_t ki = NIL;
-            const int64_t gstart = (int64_t)((base + lo) & ~3ull) - (int64_t)base;   // 4-aligned (global)
-            for (int64_t g0 = gstart + (int64_t)warp * 128; g0 < (int64_t)hi; g0 += kWarps * 128) {
-                const int64_t e0 = g0 + 4 * lane;
-                uint64_t a4[4];
-                uint32_t s4 = 0;
+            // ---- a2 + a3: stream the window, key every pending request, per-warp top-32
+            uint64_t lk = 0, kk = 0;
+            uint32_t li = NIL, ki = NIL;
+            const int64_t gstart = (int64_t)((base + lo) & ~3ull) - (int64_t)base;   // 4-aligned globally
+            const int64_t stride = (int64_t)G * 128;
+            auto load4 = [&](int64_t e0, uint64_t (&a4)[4], uint32_t& s4) {
+                s4 = 0;
                 if (e0 >= 0 && e0 + 3 < (int64_t)hi) {
                     const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(arr + e0));
                     const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(arr + e0 + 2));
-                    a4[0] = v0.x; a4[1] = v0.y; a4[2] = v1.x; a4[3] = v1.y;
+                    a4[0] = v0.x;
+                    a4[1] = v0.y;
+                    a4[2] = v1.x;
+                    a4[3] = v1.y;
                     s4 = *reinterpret_cast<const uint32_t*>(rsc + e0);
                 } else {
 #pragma unroll
@@ -310,6 +315,16 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                         s4 |= (uint32_t)(ok ? rsc[e] : 0) << (8 * j);
                     }
                 }
+            };
+            int64_t g0 = gstart + (int64_t)wg * 128;
+            uint64_t na4[4] = {0, 0, 0, 0};
+            uint32_t ns4 = 0;
+            if (g0 < (int64_t)hi) load4(g0 + 4 * lane, na4, ns4);
+            for (; g0 < (int64_t)hi; g0 += stride) {
+                uint64_t a4[4] = {na4[0], na4[1], na4[2], na4[3]};
+                const uint32_t s4 = ns4;
+                if (g0 + stride < (int64_t)hi) load4(g0 + stride + 4 * lane, na4, ns4);   // prefetch
+                const int64_t e0 = g0 + 4 * lane;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int64_t e = e0 + j;
@@ -319,7 +334,7 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                     const uint32_t id = (uint32_t)e;
                     if (valid && prio) {
                         const int c = sb & RS_CLS;
-                        const K1Class kq = c == 0 ? kc[0] : (c == 1 ? kc[1] : kc[2]);   // registers
+                        const K1Class kq = c == 0 ? kc0 : (c == 1 ? kc1 : kc2);
                         key = k1_key(kq, clock - a4[j], tb);
                     }
                     if (valid && first_pass && (sb & RS_RES)) {
@@ -329,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                             sm.partkey[slot] = key;
                         }
                     }
-                    if (valid && has_th && !before(thk, thi, key, id)) valid = false;  // already ranked
+                    if (valid && has_th && !before(thk, thi, key, id)) valid = false;   // already ranked
                     const bool enter = valid && before(key, id, kk, ki);
                     if (__any_sync(0xFFFFFFFFu, enter)) {
                         uint64_t bk = enter ? key : 0;
@@ -341,18 +356,22 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                     }
                 }
             }
-            sm.wkey[warp][lane] = lk;
-            sm.wid[warp][lane] = li;
-            __syncthreads();
+            if (G > 1) {
+                sm.wkey[wg][lane] = lk;
+                sm.wid[wg][lane] = li;
+            }
+            group_sync<G>();
 
-            // ---- a4: warp 0 merges the 8 lists and prefix-scans the admission
-            if (warp == 0) {
+            // ---- a4: warp 0 of the group merges the lists and prefix-scans the admission
+            if (wg == 0) {
+                if (G > 1) {
 #pragma unroll 1
-                for (int w = 1; w < kWarps; ++w) warp_merge(lk, li, sm.wkey[w][lane], sm.wid[w][lane], lane);
+                    for (int w = 1; w < G; ++w) warp_merge(lk, li, sm.wkey[w][lane], sm.wid[w][lane], lane);
+                }
                 const bool valid = li != NIL;
                 const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-                uint64_t left = sm.left;
-                uint64_t kv = sm.st.kv_free;
+                const uint64_t left = sm.left;
+                const uint64_t kv = sm.st.kv_free;
                 const bool blocked_prev = sm.blocked;
                 uint32_t f = 0, rr = 0, il = 0;
                 bool res = false;
@@ -391,7 +410,6 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                 const uint64_t sum_f = warp_sum64(admitted ? f : 0);
                 const uint64_t sum_inl = warp_sum64(admitted ? il : 0);
                 const bool any_misfit = __any_sync(0xFFFFFFFFu, misfit);
-                // threshold for a continuation pass = the last valid candidate of this batch
                 const int lastl = nvalid > 0 ? (int)nvalid - 1 : 0;
                 const uint64_t lastk = __shfl_sync(0xFFFFFFFFu, lk, lastl);
                 const uint32_t lasti = __shfl_sync(0xFFFFFFFFu, li, lastl);
@@ -428,8 +446,7 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                         }
                     }
                     warp_sort_desc(pk, pi, lane);
-                    // serial walk in key order (<= 3 partials under Lemma L2)
-                    for (int q = 0; q < np; ++q) {
+                    for (int q = 0; q < np; ++q) {                        // <= 3 under Lemma L2
                         const uint32_t id = __shfl_sync(0xFFFFFFFFu, pi, q);
                         if (id == NIL) break;
                         if (lane == 0 && sm.left > 0) {
@@ -449,14 +466,13 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                     if (lane == 0) sm.pass_more = 0;
                 }
             }
-            __syncthreads();
+            group_sync<G>();
             if (sm.pass_more != 1) break;
         }
 
-        // ---- a5: clock, calendar, first tokens (warp 0)
-        if (warp == 0) {
+        // ---- a5: clock, calendar, first tokens (warp 0 of the group)
+        if (wg == 0) {
             ReplicaState& st = sm.st;
-            const uint64_t n_pend0 = st.n_pend;
             if (lane == 0) {
                 if (sm.tok == 0 && st.n_dec == 0) {
                     st.status = ST_DEADLOCK;
@@ -466,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
                 st.iter++;
                 st.head[1]--;
                 st.decisions++;
-                st.sum_pending += n_pend0;
+                st.sum_pending += st.n_pend;
                 st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
                 const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};
                 cal_process(cal, t.link + base, st.iter, st.clock, fp, t.done + base, st);
@@ -505,19 +521,29 @@ __global__ void __launch_bounds__(kThreads) k_step(ModelConst m, TraceDev t, uin
             kv_add = warp_sum64(kv_add);
             n_dec_add = warp_sum64(n_dec_add);
             done_add = warp_sum64(done_add);
+            // advance the window start past served requests, 32 state bytes per probe
+            uint32_t l2 = st.head[0];
+            for (;;) {
+                const uint32_t i = l2 + lane;
+                const bool stop = i >= hi || (rs[i] & RS_PEND);
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, stop);
+                if (b) {
+                    l2 += __ffs(b) - 1;
+                    break;
+                }
+                l2 += 32;
+            }
             if (lane == 0) {
                 st.kv_free += kv_add;
                 st.n_dec += (uint32_t)n_dec_add;
                 st.done_count += (uint32_t)done_add;
-                st.n_pend -= (uint32_t)(nd);
-                uint32_t l2 = st.head[0];
-                while (l2 < st.nxt && !(rs[l2] & RS_PEND)) ++l2;    // advance the window start
-                st.head[0] = l2;
+                st.n_pend -= (uint32_t)nd;
+                st.head[0] = l2 < hi ? l2 : hi;
                 t.state[r] = st;
                 if (count_active && !(st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
             }
         }
-        __syncthreads();
+        group_sync<G>();
     }
 }
 
@@ -538,7 +564,10 @@ __global__ void k_sw_init(TraceDev t) {
 
 void stepwise_init(const TraceDev& t, cudaStream_t s) { k_sw_init<<<(t.R + 255) / 256, 256, 0, s>>>(t); }
 
-size_t stepwise_extra_bytes(uint32_t R, uint64_t N) { (void)R; return 4 * N + 16; }
+size_t stepwise_extra_bytes(uint32_t R, uint64_t N) {
+    (void)R;
+    return 4 * N + 16;
+}
 size_t stepwise_workspace_bytes(uint32_t R, uint64_t N) { return N + stepwise_extra_bytes(R, N); }
 
 StepwiseWorkspace stepwise_bind(void* p, uint32_t R) {
@@ -548,25 +577,46 @@ StepwiseWorkspace stepwise_bind(void* p, uint32_t R) {
     return w;
 }
 
-int stepwise_grid(uint32_t R) {
-    int dev = 0, sms = 148, per_sm = 1;
+namespace {
+struct Launch {
+    int grid;
+    int group;   // warps per replica
+};
+
+Launch stepwise_config(uint32_t R) {
+    int dev = 0, sms = 148, per_sm1 = 1, per_sm8 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step, kThreads, 0);
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t g = (uint64_t)sms * per_sm;
-    return (int)(R < g ? R : g);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8>, kThreads, 0);
+    if (per_sm1 < 1) per_sm1 = 1;
+    if (per_sm8 < 1) per_sm8 = 1;
+    // Warp per replica when there are enough replicas to fill every warp slot twice over;
+    // otherwise a CTA per replica so that few (large) queues still stream at full width.
+    const uint64_t warp_slots = (uint64_t)sms * per_sm1 * kWarpsPerBlock;
+    Launch l;
+    if ((uint64_t)R >= 2 * warp_slots) {
+        l.group = 1;
+        const uint64_t need = ((uint64_t)R + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        const uint64_t cap = (uint64_t)sms * per_sm1;
+        l.grid = (int)(need < cap ? need : cap);
+    } else {
+        l.group = 8;
+        const uint64_t cap = (uint64_t)sms * per_sm8;
+        l.grid = (int)((uint64_t)R < cap ? R : cap);
+    }
+    return l;
 }
+}  // namespace
 
 tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWorkspace& w, uint32_t max_iters,
                         uint32_t* d_active, cudaStream_t s, uint64_t* launches) {
     uint32_t* remv = reinterpret_cast<uint32_t*>(w.base);
-    const int grid = stepwise_grid(t.R);
-    const uint32_t budget = max_iters;
-    k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, budget);
+    const Launch L = stepwise_config(t.R);
+    k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, max_iters);
     (*launches)++;
-    // Each k_step launch advances every active replica by one iteration (or one fast-forward).
-    // Launch in chunks; read the active count only at the end of each chunk.
+    // Each k_step launch advances every active replica by one iteration (or one fast-forward);
+    // launch in chunks and read the active count only at the end of each chunk.
     const uint32_t chunk = 64;
     uint64_t done_launches = 0;
     for (;;) {
@@ -574,7 +624,9 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         if ((uint64_t)max_iters - done_launches < this_chunk) this_chunk = (uint32_t)(max_iters - done_launches);
         if (cudaMemsetAsync(d_active, 0, 4, s) != cudaSuccess) return TCM_E_CUDA;
         for (uint32_t q = 0; q < this_chunk; ++q) {
-            k_step<<<grid, kThreads, 0, s>>>(m, t, remv, d_active, q + 1 == this_chunk);
+            const int last = q + 1 == this_chunk;
+            if (L.group == 1) k_step<1><<<L.grid, kThreads, 0, s>>>(m, t, remv, d_active, last);
+            else k_step<8><<<L.grid, kThreads, 0, s>>>(m, t, remv, d_active, last);
             (*launches)++;
         }
         done_launches += this_chunk;
