@@ -176,8 +176,42 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
         }
         if (budget == 0) break;
 
-        // ---- a2 + a3 + a4: merge the class-FIFO heads by key, scan under token/KV budgets
+        // ---- Lemma L4: a blocked decision repeats identically until the next finish or arrival.
+        // Nothing can prefill when decodes take the whole budget (R8), or when no head holds KV
+        // (no partial, L2) and every class head is too large for the free KV: the top-ranked
+        // waiting request is a head (L1), its misfit stops every later admission (R6), and
+        // neither the heads nor kv_free change before a calendar finish or a new arrival.
         uint32_t left = B > st.n_dec ? B - st.n_dec : 0;   // R8
+        bool stuck = left == 0;
+        if (!stuck) {
+            stuck = true;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (st.head[c] != NIL && (((st.flags >> c) & 1u) || (uint64_t)hf[c] <= st.kv_free)) stuck = false;
+        }
+        if (stuck && st.n_dec > 0) {
+            const uint64_t F = next_fin;
+            const uint64_t dt = m.c0 + m.cd * st.n_dec;
+            uint64_t j = F - st.iter;
+            if (next_arr != ~0ull) {
+                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+                j = ja < j ? ja : j;
+            }
+            j = j < budget ? j : budget;
+            st.clock += j * dt;
+            st.iter += j;
+            st.decisions += j;
+            st.sum_pending += j * st.n_pend;
+            st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
+            budget -= (uint32_t)j;
+            if (st.iter == F) {
+                cal_process(cal, link, st.iter, st.clock, fp, done, st);
+                next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
+            }
+            continue;
+        }
+
+        // ---- a2 + a3 + a4: merge the class-FIFO heads by key, scan under token/KV budgets
         uint64_t tok = 0, inl_sum = 0;
         bool blocked = false;                               // R6
         uint32_t cur[3], crem[3], cf[3], csid[3], csf[3];

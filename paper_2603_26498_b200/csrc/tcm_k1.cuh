@@ -42,6 +42,21 @@ struct K1Tables {
 
 __device__ __forceinline__ K1Tables k1_const_tables() { return K1Tables{kLnR, kLnT, kExpT}; }
 
+// Exact integer <-> double conversions on the FMA/ALU pipes instead of the (slow, shared)
+// XU pipe: 0x1.8p52 has ulp 1, so adding it rounds to an integer (ties-to-even, i.e. rint)
+// and its low mantissa bits then hold the integer.
+constexpr double kMagic = 0x1.8p52;
+constexpr unsigned long long kMagicBits = 0x4338000000000000ull;
+
+__device__ __forceinline__ double small_int_to_double(long long e) {     // |e| < 2^51, exact
+    return __dsub_rn(__longlong_as_double((long long)(kMagicBits + (unsigned long long)e)), kMagic);
+}
+
+__device__ __forceinline__ double u64_to_double_rn(uint64_t w) {        // == __ull2double_rn(w)
+    if (w < (1ull << 52)) return __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ull | w)), 0x1p52);
+    return __ull2double_rn(w);
+}
+
 // LN(v), v a positive normal double: steps LN.1-LN.6.
 __device__ __forceinline__ double k1_ln(double v, const K1Tables& tb = k1_const_tables()) {
     const uint64_t b = (uint64_t)__double_as_longlong(v);
@@ -60,14 +75,17 @@ __device__ __forceinline__ double k1_ln(double v, const K1Tables& tb = k1_const_
     q = __fma_rn(q, u, 0x1p+0);                      // c1
     const double lnm = __dmul_rn(q, u);
     const double t = __dadd_rn(tb.lnT[j], lnm);
-    return __fma_rn((double)e, kLN2, t);
+    return __fma_rn(small_int_to_double(e), kLN2, t);
 }
 
 // EXP(y): steps EXP.1-EXP.7.
 __device__ __forceinline__ double k1_exp(double y, const K1Tables& tb = k1_const_tables()) {
     if (y < -745.0) return 0.0;
     if (y > 700.0) return __longlong_as_double(0x7FF0000000000000ll);
-    const double kf = rint(__dmul_rn(y, kInvLn2x16));
+    // EXP.2 kf = rint(y * 16/ln2) (|.| < 2^15 here, so the magic-number rounding is exact rint)
+    const double tm = __dadd_rn(__dmul_rn(y, kInvLn2x16), kMagic);
+    const double kf = __dsub_rn(tm, kMagic);
+    const long long k = (long long)((unsigned long long)__double_as_longlong(tm) - kMagicBits);
     double r = __fma_rn(-kf, kLn2d16Hi, y);
     r = __fma_rn(-kf, kLn2d16Lo, r);
     double p = 0x1.6c16c16c16c17p-10;                // 1/6!
@@ -77,7 +95,6 @@ __device__ __forceinline__ double k1_exp(double y, const K1Tables& tb = k1_const
     p = __fma_rn(p, r, 0x1p-1);                      // 1/2!
     p = __fma_rn(p, r, 0x1p+0);                      // 1/1!
     p = __fma_rn(p, r, 0x1p+0);                      // 1/0!
-    const long long k = (long long)kf;
     const long long j = k & 15;
     const long long n = (k - j) / 16;
     const double s = __dmul_rn(tb.expT[j], p);
@@ -113,7 +130,7 @@ __device__ __forceinline__ K1Class k1_class(double S, double k, double p, double
 __device__ __forceinline__ double k1_priority(const K1Class& kc, uint64_t w,
                                               const K1Tables& tb = k1_const_tables()) {
     if (w == 0 || kc.zero) return kc.S;
-    const double L = k1_ln(__ull2double_rn(w), tb);
+    const double L = k1_ln(u64_to_double_rn(w), tb);
     const double y = __fma_rn(kc.p, L, kc.C);
     const double x = k1_exp(y, tb);
     const double e = k1_exp(-x, tb);

@@ -17,8 +17,13 @@ def stage(R, pending, engine):
     sim.load(tr, res)
     return sim, res
 
-for R, pend in [(65536, 1024), (8192, 1024), (1, 100000)]:
-    for engine in (tcm.ENGINE_STEPWISE, tcm.ENGINE_FUSED):
+CONFIGS = [(65536, 1024), (8192, 1024), (1, 100000)]
+ENGINES = (tcm.ENGINE_STEPWISE, tcm.ENGINE_FUSED)
+if len(sys.argv) > 2:
+    CONFIGS = [(int(sys.argv[1]), int(sys.argv[2]))]
+    ENGINES = (tcm.ENGINE_STEPWISE,)
+for R, pend in CONFIGS:
+    for engine in ENGINES:
         sim, res = stage(R, pend, engine)
         sim.step(1)
         ts = []
@@ -32,7 +37,9 @@ for R, pend in [(65536, 1024), (8192, 1024), (1, 100000)]:
         gbs = keys * 9 / (ms / 1e3) / 1e9
         print(f"R={R} pending={pend} engine={'stepwise' if engine else 'fused'} ms/iter={ms:.4f} keys/iter={keys:.0f} eqv GB/s={gbs:.1f} ({gbs/6540.8*100:.1f}% HBM)", [round(t[0], 3) for t in ts], flush=True)
         # compare engines' results after 7 iterations
-        if engine == tcm.ENGINE_STEPWISE:
+        if len(ENGINES) == 1:
+            pass
+        elif engine == tcm.ENGINE_STEPWISE:
             ref = {k: v.clone() for k, v in res.items()}
         else:
             same = all(torch.equal(ref[k], res[k]) for k in ref)
