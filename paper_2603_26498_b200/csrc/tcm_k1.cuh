@@ -145,4 +145,65 @@ __device__ __forceinline__ uint64_t k1_key(const K1Class& kc, uint64_t w,
     return (uint64_t)__double_as_longlong(P);
 }
 
+// ---- Branch-free K1 for the streaming key kernel ------------------------------------------
+// Same spec, same operations on every in-range value, hence bit-identical results; the
+// special cases (w == 0, zero rate, EXP cut-offs, flush) are computed through and selected
+// at the end so a warp never diverges inside the key.  Coefficients live in the constant
+// bank so the DFMAs take them as c[][] operands instead of re-materialising immediates.
+__constant__ double kPoly[19] = {
+    // LN c9 .. c1
+    0x1.c71c71c71c71cp-4, -0x1p-3, 0x1.2492492492492p-3, -0x1.5555555555555p-3, 0x1.999999999999ap-3,
+    -0x1p-2, 0x1.5555555555555p-2, -0x1p-1, 0x1p+0,
+    // EXP 1/6! .. 1/0!
+    0x1.6c16c16c16c17p-10, 0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.5555555555555p-3, 0x1p-1,
+    0x1p+0, 0x1p+0,
+    // LN2, LN2/16 hi, LN2/16 lo
+    0x1.62e42fefa39efp-1, 0x1.62e42fee00000p-5, 0x1.a39ef35793c76p-37};
+
+__device__ __forceinline__ double k1_ln_bf(double v, const K1Tables& tb) {
+    const uint64_t b = (uint64_t)__double_as_longlong(v);
+    const int e = (int)((b >> 52) & 0x7FF) - 1023;
+    const int j = (int)((b >> 48) & 0xF);
+    const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+    const double u = __fma_rn(m, tb.lnR[j], -1.0);
+    double q = kPoly[0];
+#pragma unroll
+    for (int i = 1; i < 9; ++i) q = __fma_rn(q, u, kPoly[i]);
+    const double lnm = __dmul_rn(q, u);
+    const double t = __dadd_rn(tb.lnT[j], lnm);
+    return __fma_rn(small_int_to_double(e), kPoly[16], t);
+}
+
+__device__ __forceinline__ double k1_exp_bf(double y, const K1Tables& tb) {
+    const double yc = fmin(fmax(y, -746.0), 701.0);         // keeps the discarded lanes finite
+    const double tm = __dadd_rn(__dmul_rn(yc, kInvLn2x16), kMagic);
+    const double kf = __dsub_rn(tm, kMagic);
+    const long long k = (long long)((unsigned long long)__double_as_longlong(tm) - kMagicBits);
+    double r = __fma_rn(-kf, kPoly[17], yc);
+    r = __fma_rn(-kf, kPoly[18], r);
+    double p = kPoly[9];
+#pragma unroll
+    for (int i = 10; i < 16; ++i) p = __fma_rn(p, r, kPoly[i]);
+    const int j = (int)(k & 15);
+    const long long n = k >> 4;                               // == (k - j) / 16 exactly
+    const double s = __dmul_rn(tb.expT[j], p);
+    const long long nn = n < -1021 ? -1021 : n;               // discarded when n < -1021
+    double res = __dmul_rn(s, __longlong_as_double((long long)((unsigned long long)(nn + 1023) << 52)));
+    res = (n < -1021 || res < 0x1p-1022) ? 0.0 : res;
+    res = y < -745.0 ? 0.0 : res;
+    return y > 700.0 ? __longlong_as_double(0x7FF0000000000000ll) : res;
+}
+
+__device__ __forceinline__ uint64_t k1_key_bf(double S, double p, double C, bool zero, uint64_t w,
+                                              const K1Tables& tb) {
+    const double L = k1_ln_bf(u64_to_double_rn(w), tb);
+    const double y = __fma_rn(p, L, C);
+    const double x = k1_exp_bf(y, tb);
+    const double e = k1_exp_bf(-x, tb);
+    double P = __dadd_rn(S, __dsub_rn(1.0, e));
+    P = (w == 0 || zero) ? S : P;
+    P = P < kEps ? kEps : P;
+    return (uint64_t)__double_as_longlong(P);
+}
+
 }  // namespace tcm

@@ -321,38 +321,55 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             uint32_t ns4 = 0;
             if (g0 < (int64_t)hi) load4(g0 + 4 * lane, na4, ns4);
             for (; g0 < (int64_t)hi; g0 += stride) {
-                uint64_t a4[4] = {na4[0], na4[1], na4[2], na4[3]};
+                const uint64_t a4[4] = {na4[0], na4[1], na4[2], na4[3]};
                 const uint32_t s4 = ns4;
                 if (g0 + stride < (int64_t)hi) load4(g0 + stride + 4 * lane, na4, ns4);   // prefetch
-                const int64_t e0 = g0 + 4 * lane;
+                const int e0 = (int)(g0 + 4 * lane);
+                uint64_t key[4];
+                bool valid[4];
+                bool any_res = false, any_enter = false;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int64_t e = e0 + j;
+                for (int j = 0; j < 4; ++j) {                     // branch-free keys
+                    const int e = e0 + j;
                     const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                    bool valid = e >= (int64_t)lo && e < (int64_t)hi && (sb & RS_PEND);
-                    uint64_t key = 0;
-                    const uint32_t id = (uint32_t)e;
-                    if (valid && prio) {
-                        const int c = sb & RS_CLS;
-                        const K1Class kq = c == 0 ? kc0 : (c == 1 ? kc1 : kc2);
-                        key = k1_key(kq, clock - a4[j], tb);
-                    }
-                    if (valid && first_pass && (sb & RS_RES)) {
-                        const int slot = atomicAdd(&sm.npart, 1);
-                        if (slot < kMaxPart) {
-                            sm.part[slot] = id;
-                            sm.partkey[slot] = key;
+                    valid[j] = e >= (int)lo && e < (int)hi && (sb & RS_PEND);
+                    const int c = sb & RS_CLS;
+                    const double S = c == 0 ? kc0.S : (c == 1 ? kc1.S : kc2.S);
+                    const double P = c == 0 ? kc0.p : (c == 1 ? kc1.p : kc2.p);
+                    const double C = c == 0 ? kc0.C : (c == 1 ? kc1.C : kc2.C);
+                    const bool Z = c == 0 ? kc0.zero : (c == 1 ? kc1.zero : kc2.zero);
+                    key[j] = prio ? k1_key_bf(S, P, C, Z, clock - a4[j], tb) : 0;
+                    any_res |= valid[j] && (sb & RS_RES);
+                    if (has_th && !before(thk, thi, key[j], (uint32_t)e)) valid[j] = false;   // already ranked
+                    any_enter |= valid[j] && before(key[j], (uint32_t)e, kk, ki);
+                }
+                if (first_pass && __any_sync(0xFFFFFFFFu, any_res)) {    // partials: rare (<= 3, L2)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int e = e0 + j;
+                        const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
+                        if (e >= (int)lo && e < (int)hi && (sb & RS_PEND) && (sb & RS_RES)) {
+                            const int slot = atomicAdd(&sm.npart, 1);
+                            if (slot < kMaxPart) {
+                                sm.part[slot] = (uint32_t)e;
+                                sm.partkey[slot] = key[j];
+                            }
                         }
                     }
-                    if (valid && has_th && !before(thk, thi, key, id)) valid = false;   // already ranked
-                    const bool enter = valid && before(key, id, kk, ki);
-                    if (__any_sync(0xFFFFFFFFu, enter)) {
-                        uint64_t bk = enter ? key : 0;
-                        uint32_t bi = enter ? id : NIL;
-                        warp_sort_desc(bk, bi, lane);
-                        warp_merge(lk, li, bk, bi, lane);
-                        kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
-                        ki = __shfl_sync(0xFFFFFFFFu, li, 31);
+                }
+                if (__any_sync(0xFFFFFFFFu, any_enter)) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t id = (uint32_t)(e0 + j);
+                        const bool enter = valid[j] && before(key[j], id, kk, ki);
+                        if (__any_sync(0xFFFFFFFFu, enter)) {
+                            uint64_t bk = enter ? key[j] : 0;
+                            uint32_t bi = enter ? id : NIL;
+                            warp_sort_desc(bk, bi, lane);
+                            warp_merge(lk, li, bk, bi, lane);
+                            kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
+                            ki = __shfl_sync(0xFFFFFFFFu, li, 31);
+                        }
                     }
                 }
             }
