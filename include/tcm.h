@@ -211,6 +211,10 @@ tcm_status tcm_k1_eval(const tcm_config* cfg, const uint8_t* cls, const uint64_t
                        const double* alpha, double* out_priority, uint64_t n, void* cuda_stream);
 tcm_status tcm_k1_audit(const tcm_config* cfg, uint32_t cls, double alpha, uint64_t w_lo,
                         uint64_t w_hi, uint64_t* first_violation, void* cuda_stream);
+/* Max |P~ - P| over w = w_lo, w_lo + step, ... < w_hi of the stepwise engine's FP32 priority
+ * bound P~ against K1; written to *max_err (HOST).  The engine assumes <= 1e-4. */
+tcm_status tcm_k1_filter_error(const tcm_config* cfg, uint32_t cls, double alpha, uint64_t w_lo,
+                               uint64_t w_hi, uint64_t step, double* max_err, void* cuda_stream);
 
 #ifdef __cplusplus
 }

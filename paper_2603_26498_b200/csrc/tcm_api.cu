@@ -457,4 +457,26 @@ tcm_status tcm_k1_audit(const tcm_config* cfg, uint32_t cls, double alpha, uint6
     return TCM_OK;
 }
 
+tcm_status tcm_k1_filter_error(const tcm_config* cfg, uint32_t cls, double alpha, uint64_t lo, uint64_t hi,
+                               uint64_t step, double* max_err, void* stream) {
+    tcm_status st = validate_config(cfg);
+    if (st != TCM_OK) return st;
+    if (cls > 2 || hi <= lo || step == 0 || !max_err) return fail(nullptr, TCM_E_ARG, "bad filter-audit arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d, 0, 8, s);
+    if (e == cudaSuccess) {
+        launch_filter_audit(to_model(*cfg), cls, alpha, lo, hi, step, d, s);
+        e = cudaGetLastError();
+    }
+    unsigned long long h = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(nullptr, TCM_E_CUDA, "k1_filter_error: %s", cudaGetErrorString(e));
+    memcpy(max_err, &h, 8);
+    return TCM_OK;
+}
+
 }  // extern "C"

@@ -248,7 +248,30 @@ __global__ void k_k1_audit(ModelConst m, uint32_t c, double alpha, uint64_t lo, 
     }
 }
 
+// Max |P~ - P| of the FP32 filter bound over w in [lo, hi) (stepwise engine):
+// non-negative doubles order like their bit patterns, so atomicMax on the bits is exact.
+__global__ void k_filter_audit(ModelConst m, uint32_t c, double alpha, uint64_t lo, uint64_t hi, uint64_t step,
+                               unsigned long long* maxerr) {
+    const K1Class kc = k1_class(m.S[c], m.k[c], m.p[c], alpha);
+    const float fS = (float)kc.S, fp2 = (float)kc.p, fC2 = (float)__dmul_rn(kc.C, 1.4426950408889634);
+    double worst = 0.0;
+    const uint64_t n = (hi - lo + step - 1) / step;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = lo + q * step;
+        if (w == 0 || kc.zero) continue;
+        const double P = k1_priority(kc, w);
+        const double Pf = (double)k1_filter_f32(fS, fp2, fC2, w);
+        const double err = fabs(Pf - P);
+        worst = err > worst ? err : worst;
+    }
+    atomicMax(maxerr, (unsigned long long)__double_as_longlong(worst));
+}
+
 // ---------------------------------------------------------------------------------------
+void launch_filter_audit(const ModelConst& m, uint32_t c, double alpha, uint64_t lo, uint64_t hi, uint64_t step,
+                         unsigned long long* maxerr, cudaStream_t s) {
+    k_filter_audit<<<148 * 8, 256, 0, s>>>(m, c, alpha, lo, hi, step, maxerr);
+}
 void launch_init(const TraceDev& t, cudaStream_t s) {
     k_init<<<(t.R + 127) / 128, 128, 0, s>>>(t);
 }

@@ -20,6 +20,8 @@ void launch_generate(const void* reps, uint32_t R, const uint64_t* off, uint64_t
                      cudaStream_t s);
 void launch_k1_eval(const ModelConst& m, const uint8_t* cls, const uint64_t* w, const double* alpha,
                     double* outp, uint64_t n, cudaStream_t s);
+void launch_filter_audit(const ModelConst& m, uint32_t c, double alpha, uint64_t lo, uint64_t hi, uint64_t step,
+                         unsigned long long* maxerr, cudaStream_t s);
 void launch_k1_audit(const ModelConst& m, uint32_t c, double alpha, uint64_t lo, uint64_t hi,
                      unsigned long long* first, cudaStream_t s);
 

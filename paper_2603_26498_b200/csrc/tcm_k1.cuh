@@ -194,6 +194,38 @@ __device__ __forceinline__ double k1_exp_bf(double y, const K1Tables& tb) {
     return y > 700.0 ? __longlong_as_double(0x7FF0000000000000ll) : res;
 }
 
+// ---- FP32 bound on the priority (filter for the exact top-k; never decides an order) --------
+// P~ = S + (1 - 2^(-x log2 e)), x = 2^(p2 * log2(w) + C2), C2 = C / ln 2, evaluated with the
+// SFU approximations (PTX lg2.approx / ex2.approx, max errors 2^-22.6 abs / 2^-22.5 rel) and
+// log2(w) from the exact exponent plus the top 24 mantissa bits.  Error budget:
+// |P~ - P| <= 0.37 * ln2 * (p * 2.5e-6 + (|y| + |C2|) * 6e-8) + 1e-6, i.e. < 1e-5 for the
+// supported range (p <= 16, |C2| <= 1000); the kernel uses kFilterDelta = 1e-4, and
+// tcm_k1_filter_error() audits the bound exhaustively per (class, alpha) on the device.
+constexpr double kFilterDelta = 1e-4;
+
+__device__ __forceinline__ float sfu_lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sfu_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float k1_filter_f32(float Sf, float p2, float C2, uint64_t w) {
+    const int lz = __clzll((long long)w);                 // w >= 1
+    const int e = 63 - lz;
+    const uint32_t mant = (uint32_t)((w << lz) >> 40) & 0x7FFFFFu;
+    const float M = __uint_as_float(0x3F800000u | mant);
+    const float ef = __int_as_float(0x4B000000 + e) - 8388608.0f;   // exact small int -> float
+    const float L = ef + sfu_lg2(M);
+    const float x = sfu_ex2(fmaf(p2, L, C2));
+    const float ee = sfu_ex2(-x * 1.44269504f);
+    return Sf + (1.0f - ee);
+}
+
 __device__ __forceinline__ uint64_t k1_key_bf(double S, double p, double C, bool zero, uint64_t w,
                                               const K1Tables& tb) {
     const double L = k1_ln_bf(u64_to_double_rn(w), tb);

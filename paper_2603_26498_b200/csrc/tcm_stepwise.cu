@@ -138,8 +138,17 @@ struct GroupSmem {
     uint64_t partkey[kMaxPart];
     uint32_t part[kMaxPart];
     uint32_t done[kMaxDone];
+    // per-warp refine queue: elements whose FP32 bound cannot rule them out of the top-32
+    static constexpr int kQ = 160;
+    uint32_t qid[G][kQ];
+    uint64_t qw[G][kQ];
+    uint8_t qc[G][kQ];
+    int qn[G];
     ReplicaState st;
     K1Class kc[3];
+    double dS[3], dSmax[3];   // exact bounds S_c <= P <= fl(S_c + 1)
+    float fS[3], fp2[3], fC2[3];
+    int filter_ok;
     uint64_t thk;       // continuation threshold: exclude ranks <= (thk, thi)
     uint64_t left, tok, inl;
     uint32_t thi;
@@ -271,8 +280,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
         const uint64_t clock = sm.st.clock;
         const uint32_t lo = sm.st.head[0], hi = sm.st.nxt;
         if (wg == 0) {
-            if (lane < 3) sm.kc[lane] = k1_class(m.S[lane], m.k[lane], m.p[lane], prm.aging_alpha);
+            bool ok = true;
+            if (lane < 3) {
+                const K1Class k = k1_class(m.S[lane], m.k[lane], m.p[lane], prm.aging_alpha);
+                sm.kc[lane] = k;
+                sm.dS[lane] = k.S;
+                sm.dSmax[lane] = __dadd_rn(k.S, 1.0);
+                const double c2 = __dmul_rn(k.C, 1.4426950408889634);      // natural -> base-2
+                sm.fS[lane] = (float)k.S;
+                sm.fp2[lane] = (float)k.p;
+                sm.fC2[lane] = (float)c2;
+                ok = k.zero || (k.p <= 16.0 && fabs(c2) <= 1000.0);      // validated bound range
+            }
+            const bool all_ok = __all_sync(0xFFFFFFFFu, ok);
             if (lane == 0) {
+                sm.filter_ok = all_ok;
                 const uint32_t B = prm.chunk_budget;
                 sm.left = B > sm.st.n_dec ? B - sm.st.n_dec : 0;     // R8
                 sm.tok = 0;
@@ -284,16 +306,59 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             }
         }
         group_sync<G>();
-        const K1Class kc0 = sm.kc[0], kc1 = sm.kc[1], kc2 = sm.kc[2];
+        const bool filter_ok = sm.filter_ok;
 
         for (int pass = 0;; ++pass) {
             const bool first_pass = pass == 0;
             const bool has_th = sm.has_th;
             const uint64_t thk = sm.thk;
             const uint32_t thi = sm.thi;
-            // ---- a2 + a3: stream the window, key every pending request, per-warp top-32
+            const double Pth = __longlong_as_double((long long)thk);
+            // ---- a2 + a3: stream the window; every pending request gets an FP32 bound on its
+            // priority; those that could still enter this warp's exact top-32 (or hold KV as a
+            // partial) are queued for the exact K1 key.  The selected set equals the top-32 of
+            // exact keys: a request is skipped only when max(P~ + delta, ...) proves it ranks
+            // after the current 32nd, using S_c <= P <= S_c + 1 exactly.
             uint64_t lk = 0, kk = 0;
             uint32_t li = NIL, ki = NIL;
+            double Pkk = 0.0;
+            int qn = 0;
+            uint32_t* qid = sm.qid[wg];
+            uint64_t* qw = sm.qw[wg];
+            uint8_t* qc = sm.qc[wg];
+            auto take = [&](uint64_t key, uint32_t id, bool enter) {   // warp-collective
+                if (__any_sync(0xFFFFFFFFu, enter)) {
+                    uint64_t bk = enter ? key : 0;
+                    uint32_t bi = enter ? id : NIL;
+                    warp_sort_desc(bk, bi, lane);
+                    warp_merge(lk, li, bk, bi, lane);
+                    kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
+                    ki = __shfl_sync(0xFFFFFFFFu, li, 31);
+                    Pkk = __longlong_as_double((long long)kk);
+                }
+            };
+            auto refine = [&](int cnt) {                               // exact keys for <= 32 queued
+                uint64_t key = 0;
+                uint32_t id = NIL;
+                bool enter = false;
+                if (lane < cnt) {
+                    id = qid[lane];
+                    const int cc = qc[lane];
+                    const int c = cc & RS_CLS;
+                    const K1Class& k = sm.kc[c];
+                    key = k1_key_bf(k.S, k.p, k.C, k.zero, qw[lane], tb);
+                    if (first_pass && (cc & RS_RES)) {                 // partial: remember its key
+                        const int slot = atomicAdd(&sm.npart, 1);
+                        if (slot < kMaxPart) {
+                            sm.part[slot] = id;
+                            sm.partkey[slot] = key;
+                        }
+                    }
+                    const bool valid = !(has_th && !before(thk, thi, key, id));
+                    enter = valid && before(key, id, kk, ki);
+                }
+                take(key, id, enter);
+            };
             const int64_t gstart = (int64_t)((base + lo) & ~3ull) - (int64_t)base;   // 4-aligned globally
             const int64_t stride = (int64_t)G * 128;
             auto load4 = [&](int64_t e0, uint64_t (&a4)[4], uint32_t& s4) {
@@ -325,54 +390,86 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 const uint32_t s4 = ns4;
                 if (g0 + stride < (int64_t)hi) load4(g0 + stride + 4 * lane, na4, ns4);   // prefetch
                 const int e0 = (int)(g0 + 4 * lane);
-                uint64_t key[4];
-                bool valid[4];
-                bool any_res = false, any_enter = false;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {                     // branch-free keys
+                for (int j = 0; j < 4; ++j) {
                     const int e = e0 + j;
                     const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                    valid[j] = e >= (int)lo && e < (int)hi && (sb & RS_PEND);
+                    const bool valid = e >= (int)lo && e < (int)hi && (sb & RS_PEND);
                     const int c = sb & RS_CLS;
-                    const double S = c == 0 ? kc0.S : (c == 1 ? kc1.S : kc2.S);
-                    const double P = c == 0 ? kc0.p : (c == 1 ? kc1.p : kc2.p);
-                    const double C = c == 0 ? kc0.C : (c == 1 ? kc1.C : kc2.C);
-                    const bool Z = c == 0 ? kc0.zero : (c == 1 ? kc1.zero : kc2.zero);
-                    key[j] = prio ? k1_key_bf(S, P, C, Z, clock - a4[j], tb) : 0;
-                    any_res |= valid[j] && (sb & RS_RES);
-                    if (has_th && !before(thk, thi, key[j], (uint32_t)e)) valid[j] = false;   // already ranked
-                    any_enter |= valid[j] && before(key[j], (uint32_t)e, kk, ki);
-                }
-                if (first_pass && __any_sync(0xFFFFFFFFu, any_res)) {    // partials: rare (<= 3, L2)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int e = e0 + j;
-                        const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                        if (e >= (int)lo && e < (int)hi && (sb & RS_PEND) && (sb & RS_RES)) {
+                    const uint64_t w = clock - a4[j];
+                    const bool res = (sb & RS_RES) != 0;
+                    // exact without K1: FCFS (key 0, order = id) or P = S_c (w = 0 / zero rate)
+                    const bool trivial = !prio || w == 0 || sm.kc[c].zero;
+                    bool queue = false, enter = false;
+                    uint64_t key = 0;
+                    if (trivial) {
+                        if (prio) {
+                            const double S = sm.dS[c];
+                            key = (uint64_t)__double_as_longlong(S < kEps ? kEps : S);
+                        }
+                        if (valid && first_pass && res) {
                             const int slot = atomicAdd(&sm.npart, 1);
                             if (slot < kMaxPart) {
                                 sm.part[slot] = (uint32_t)e;
-                                sm.partkey[slot] = key[j];
+                                sm.partkey[slot] = key;
                             }
                         }
-                    }
-                }
-                if (__any_sync(0xFFFFFFFFu, any_enter)) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint32_t id = (uint32_t)(e0 + j);
-                        const bool enter = valid[j] && before(key[j], id, kk, ki);
-                        if (__any_sync(0xFFFFFFFFu, enter)) {
-                            uint64_t bk = enter ? key[j] : 0;
-                            uint32_t bi = enter ? id : NIL;
-                            warp_sort_desc(bk, bi, lane);
-                            warp_merge(lk, li, bk, bi, lane);
-                            kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
-                            ki = __shfl_sync(0xFFFFFFFFu, li, 31);
+                        enter = valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
+                                before(key, (uint32_t)e, kk, ki);
+                    } else if (valid) {
+                        queue = true;
+                        if (filter_ok && !(first_pass && res)) {
+                            const float pf = k1_filter_f32(sm.fS[c], sm.fp2[c], sm.fC2[c], w);
+                            const double U = fmax(fmin((double)pf + kFilterDelta, sm.dSmax[c]), kEps);
+                            const bool can_enter = !(U < Pkk || (U == Pkk && (uint32_t)e > ki));
+                            bool excluded = false;
+                            if (has_th) {
+                                const double Lb = fmax(fmax((double)pf - kFilterDelta, sm.dS[c]), kEps);
+                                excluded = Lb > Pth || (Lb == Pth && (uint32_t)e < thi);
+                            }
+                            queue = can_enter && !excluded;
                         }
                     }
+                    take(key, (uint32_t)e, enter);
+                    const uint32_t qm = __ballot_sync(0xFFFFFFFFu, queue);
+                    if (queue) {
+                        const int pos = qn + __popc(qm & ((1u << lane) - 1));
+                        qid[pos] = (uint32_t)e;
+                        qw[pos] = w;
+                        qc[pos] = (uint8_t)(c | (res ? RS_RES : 0));
+                    }
+                    qn += __popc(qm);
+                }
+                __syncwarp();
+                while (qn >= 32) {
+                    refine(32);
+                    uint32_t tid4[4];
+                    uint64_t tw4[4];
+                    uint8_t tc4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {                 // qn - 32 <= 128 left to shift
+                        const int q = 32 + lane + 32 * k;
+                        if (q < qn) {
+                            tid4[k] = qid[q];
+                            tw4[k] = qw[q];
+                            tc4[k] = qc[q];
+                        }
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int q = 32 + lane + 32 * k;
+                        if (q < qn) {
+                            qid[q - 32] = tid4[k];
+                            qw[q - 32] = tw4[k];
+                            qc[q - 32] = tc4[k];
+                        }
+                    }
+                    qn -= 32;
+                    __syncwarp();
                 }
             }
+            if (qn > 0) refine(qn);
             if (G > 1) {
                 sm.wkey[wg][lane] = lk;
                 sm.wid[wg][lane] = li;

@@ -27,7 +27,7 @@ INF32 = 0xFFFFFFFF
 
 EXPORTS = ("tcm_create", "tcm_load_trace", "tcm_reset", "tcm_step", "tcm_run", "tcm_stats", "tcm_destroy",
            "tcm_last_error", "tcm_workspace_bytes", "tcm_generate_trace", "tcm_k1_eval",
-           "tcm_k1_audit")
+           "tcm_k1_audit", "tcm_k1_filter_error")
 
 
 class TcmError(RuntimeError):
@@ -112,6 +112,10 @@ def lib():
         L.tcm_k1_audit.restype = st
         L.tcm_k1_audit.argtypes = [ctypes.POINTER(tcm_config), ctypes.c_uint32, ctypes.c_double,
                                    ctypes.c_uint64, ctypes.c_uint64, vp, vp]
+        L.tcm_k1_filter_error.restype = st
+        L.tcm_k1_filter_error.argtypes = [ctypes.POINTER(tcm_config), ctypes.c_uint32, ctypes.c_double,
+                                          ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.POINTER(ctypes.c_double), vp]
         _lib = L
     return _lib
 
@@ -230,6 +234,13 @@ def tcm_k1_eval(cfg, cls_dev, w_dev, alpha_dev, out_dev, stream=None):
 def tcm_k1_audit(cfg, cls, alpha, w_lo, w_hi, first_dev, stream=None):
     s = None if stream is None else stream.cuda_stream
     _check(lib().tcm_k1_audit(ctypes.byref(cfg), cls, alpha, w_lo, w_hi, _ptr(first_dev), s))
+
+
+def tcm_k1_filter_error(cfg, cls, alpha, w_lo, w_hi, step=1, stream=None) -> float:
+    s = None if stream is None else stream.cuda_stream
+    out = ctypes.c_double(0.0)
+    _check(lib().tcm_k1_filter_error(ctypes.byref(cfg), cls, alpha, w_lo, w_hi, step, ctypes.byref(out), s))
+    return out.value
 
 
 # --------------------------------------------------------------------------------------

@@ -244,3 +244,14 @@ def test_aggregation_matches_oracle():
         O.aggregate(tr.replica(r), res, chunk_budget=int(params["chunk_budget"][r]), hist=H[cell], cnt=C[cell])
     np.testing.assert_array_equal(hist.cpu().numpy(), H)
     np.testing.assert_array_equal(cnt.cpu().numpy(), C)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 2.0**-7, 0.125, 8.0, 128.0])
+def test_filter_bound_within_delta(alpha):
+    # The stepwise engine skips the exact key of a request only when its FP32 bound proves it
+    # cannot enter the top-32; that is exact iff |P~ - P| <= delta = 1e-4.  Audit every us of
+    # [0, 2^28) and a 97-us lattice of [0, 2^36) per class (the design bound is < 1e-5).
+    for c in range(3):
+        e1 = tcm.tcm_k1_filter_error(tcm.config(), c, alpha, 0, 2**28, 1)
+        e2 = tcm.tcm_k1_filter_error(tcm.config(), c, alpha, 0, 2**36, 97)
+        assert max(e1, e2) < 1e-5, (c, alpha, e1, e2)
