@@ -110,7 +110,8 @@ size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) 
     b += 4 * N;                                  // link
     b += (size_t)R * kCalSlots * 4;              // calendar heads
     b += (size_t)R * kCalWords * 4;              // occupancy
-    b += (size_t)R * sizeof(ReplicaState);
+ b += (size_t)R * sizeof(ReplicaState);
+    b += (size_t)R * sizeof(ClassPack);
     b += 20 * N;                                 // results kept on device when not supplied
     if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N);
     if (host_mirror) b += (size_t)(R + 1) * 8 + 19 * N + (size_t)R * sizeof(tcm_replica_params);
@@ -286,6 +287,8 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     t.occ = (uint32_t*)p;
     if ((st = dalloc(c, &p, (size_t)R * sizeof(ReplicaState)))) return st;
     t.state = (ReplicaState*)p;
+    if ((st = dalloc(c, &p, (size_t)R * sizeof(ClassPack)))) return st;
+    t.kpack = (ClassPack*)p;
     if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
         if ((st = dalloc(c, &p, N ? N : 1))) return st;
         t.req_state = (uint8_t*)p;
@@ -312,6 +315,9 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     if (hv[0] != ST_OK)
         return fail(c, TCM_E_ARG, "replica %u: malformed trace or params (footprint/out/modality/"
                     "arrival order/policy/budget/kv/alpha)", hv[1]);
+    launch_kpack(c->m, t, s);                 // params are validated: K1 class constants once
+    c->launches++;
+    TCM_CUDA(c, cudaGetLastError());
     c->loaded = true;
     c->err.clear();
     return TCM_OK;

@@ -38,6 +38,32 @@ __global__ void k_init(TraceDev t) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Per-replica K1 class constants (once per load).
+__global__ void k_kpack(ModelConst m, TraceDev t) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= t.R) return;
+    const double alpha = t.params[r].aging_alpha;
+    ClassPack kp;
+    kp.zero_mask = 0;
+    kp.filter_ok = 1;
+    for (int c = 0; c < 3; ++c) {
+        const K1Class k = k1_class(m.S[c], m.k[c], m.p[c], alpha);
+        kp.S[c] = k.S;
+        kp.p[c] = k.p;
+        kp.C[c] = k.C;
+        kp.Smax[c] = k.zero ? k.S : __dadd_rn(k.S, 1.0);
+        const double c2 = __dmul_rn(k.C, 1.4426950408889634);
+        kp.fS[c] = (float)k.S;
+        kp.fp2[c] = (float)k.p;
+        kp.fC2[c] = (float)c2;
+        if (k.zero) kp.zero_mask |= 1u << c;
+        else if (!(k.p <= 16.0 && fabs(c2) <= 1000.0)) kp.filter_ok = 0;
+    }
+    kp.pad = 0;
+    t.kpack[r] = kp;
+}
+
+// ---------------------------------------------------------------------------------------
 // Validation: one warp per replica, lanes stride its requests (coalesced).
 // v[0] = worst status code (max), v[1] = first bad replica (min).
 __global__ void k_validate(TraceDev t, uint32_t* v) {
@@ -271,6 +297,9 @@ __global__ void k_filter_audit(ModelConst m, uint32_t c, double alpha, uint64_t 
 void launch_filter_audit(const ModelConst& m, uint32_t c, double alpha, uint64_t lo, uint64_t hi, uint64_t step,
                          unsigned long long* maxerr, cudaStream_t s) {
     k_filter_audit<<<148 * 8, 256, 0, s>>>(m, c, alpha, lo, hi, step, maxerr);
+}
+void launch_kpack(const ModelConst& m, const TraceDev& t, cudaStream_t s) {
+    k_kpack<<<(t.R + 127) / 128, 128, 0, s>>>(m, t);
 }
 void launch_init(const TraceDev& t, cudaStream_t s) {
     k_init<<<(t.R + 127) / 128, 128, 0, s>>>(t);

@@ -44,6 +44,17 @@ static_assert(sizeof(ReplicaState) == 128, "ReplicaState must be one 128-byte li
 
 constexpr uint32_t FLAG_FINISHED = 1u << 8;
 
+// Per-replica K1 class constants, computed once per tcm_load_trace.
+struct __align__(16) ClassPack {
+    double S[3], p[3], C[3];   // K1 inputs: StaticPriority, p_c, C_c = LN(alpha k_c) - p_c LN(1e6)
+    double Smax[3];            // exact upper bound of P: fl(S_c + 1), or S_c for a zero-rate class
+    float fS[3], fp2[3], fC2[3];   // FP32 bound inputs (C2 = C / ln 2)
+    uint32_t zero_mask;        // bit c: alpha * k_c == 0 (P == S_c)
+    uint32_t filter_ok;        // FP32 bound validated for these constants (p <= 16, |C2| <= 1000)
+    uint32_t pad;
+};
+static_assert(sizeof(ClassPack) == 144, "ClassPack layout");
+
 // Model constants in the kernels' parameter space.
 struct ModelConst {
     uint64_t c0, cp, cd;
@@ -73,6 +84,7 @@ struct TraceDev {
     uint32_t* occ;           // [R * kCalWords] calendar occupancy bits
     ReplicaState* state;     // [R]
     uint8_t* req_state;      // [N] stepwise engine: per-request class / phase byte
+    ClassPack* kpack;        // [R] per-replica K1 class constants
 };
 
 __device__ __forceinline__ int classify(const ModelConst& m, uint32_t mod, uint32_t f) {

@@ -145,10 +145,7 @@ struct GroupSmem {
     uint8_t qc[G][kQ];
     int qn[G];
     ReplicaState st;
-    K1Class kc[3];
-    double dS[3], dSmax[3];   // exact bounds S_c <= P <= fl(S_c + 1)
-    float fS[3], fp2[3], fC2[3];
-    int filter_ok;
+    ClassPack kp;       // per-replica K1 class constants (precomputed at load)
     uint64_t thk;       // continuation threshold: exclude ranks <= (thk, thi)
     uint64_t left, tok, inl;
     uint32_t thi;
@@ -280,21 +277,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
         const uint64_t clock = sm.st.clock;
         const uint32_t lo = sm.st.head[0], hi = sm.st.nxt;
         if (wg == 0) {
-            bool ok = true;
-            if (lane < 3) {
-                const K1Class k = k1_class(m.S[lane], m.k[lane], m.p[lane], prm.aging_alpha);
-                sm.kc[lane] = k;
-                sm.dS[lane] = k.S;
-                sm.dSmax[lane] = __dadd_rn(k.S, 1.0);
-                const double c2 = __dmul_rn(k.C, 1.4426950408889634);      // natural -> base-2
-                sm.fS[lane] = (float)k.S;
-                sm.fp2[lane] = (float)k.p;
-                sm.fC2[lane] = (float)c2;
-                ok = k.zero || (k.p <= 16.0 && fabs(c2) <= 1000.0);      // validated bound range
+            {   // stage the replica's ClassPack (144 B) in shared memory
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(t.kpack + r);
+                uint32_t* dst = reinterpret_cast<uint32_t*>(&sm.kp);
+                for (int q = lane; q < (int)(sizeof(ClassPack) / 4); q += 32) dst[q] = src[q];
             }
-            const bool all_ok = __all_sync(0xFFFFFFFFu, ok);
             if (lane == 0) {
-                sm.filter_ok = all_ok;
                 const uint32_t B = prm.chunk_budget;
                 sm.left = B > sm.st.n_dec ? B - sm.st.n_dec : 0;     // R8
                 sm.tok = 0;
@@ -306,7 +294,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             }
         }
         group_sync<G>();
-        const bool filter_ok = sm.filter_ok;
+        const bool filter_ok = sm.kp.filter_ok != 0;
+        const uint32_t zero_mask = sm.kp.zero_mask;
 
         for (int pass = 0;; ++pass) {
             const bool first_pass = pass == 0;
@@ -321,7 +310,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             // after the current 32nd, using S_c <= P <= S_c + 1 exactly.
             uint64_t lk = 0, kk = 0;
             uint32_t li = NIL, ki = NIL;
-            double Pkk = 0.0;
+            // threshold state derived from the warp's current 32nd (kk, ki): a float lower bound
+            // of its priority and the classes whose exact cap S_c <= P <= Smax_c rules them out
+            float thrf = 0.0f;
+            uint32_t skipm = 0, tiem = 0;
+            auto retune = [&]() {
+                const double Pkk = __longlong_as_double((long long)kk);
+                thrf = __double2float_rd(Pkk);
+                skipm = 0;
+                tiem = 0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double cap = sm.kp.Smax[c] < kEps ? kEps : sm.kp.Smax[c];
+                    if (cap < Pkk) skipm |= 1u << c;
+                    else if (cap == Pkk) tiem |= 1u << c;
+                }
+            };
             int qn = 0;
             uint32_t* qid = sm.qid[wg];
             uint64_t* qw = sm.qw[wg];
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     warp_merge(lk, li, bk, bi, lane);
                     kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
                     ki = __shfl_sync(0xFFFFFFFFu, li, 31);
-                    Pkk = __longlong_as_double((long long)kk);
+                    retune();
                 }
             };
             auto refine = [&](int cnt) {                               // exact keys for <= 32 queued
@@ -345,8 +349,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     id = qid[lane];
                     const int cc = qc[lane];
                     const int c = cc & RS_CLS;
-                    const K1Class& k = sm.kc[c];
-                    key = k1_key_bf(k.S, k.p, k.C, k.zero, qw[lane], tb);
+                    key = prio ? k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qw[lane], tb) : 0;
                     if (first_pass && (cc & RS_RES)) {                 // partial: remember its key
                         const int slot = atomicAdd(&sm.npart, 1);
                         if (slot < kMaxPart) {
@@ -359,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 }
                 take(key, id, enter);
             };
+            const bool lean = prio && filter_ok && !has_th;    // FP32-bound path (else: exact for all)
             const int64_t gstart = (int64_t)((base + lo) & ~3ull) - (int64_t)base;   // 4-aligned globally
             const int64_t stride = (int64_t)G * 128;
             auto load4 = [&](int64_t e0, uint64_t (&a4)[4], uint32_t& s4) {
@@ -390,83 +394,90 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 const uint32_t s4 = ns4;
                 if (g0 + stride < (int64_t)hi) load4(g0 + stride + 4 * lane, na4, ns4);   // prefetch
                 const int e0 = (int)(g0 + 4 * lane);
+                uint32_t qbits = 0;                       // bit j: element j goes to the refine queue
+                bool any_direct = false;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int e = e0 + j;
                     const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                    const bool valid = e >= (int)lo && e < (int)hi && (sb & RS_PEND);
+                    const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
                     const int c = sb & RS_CLS;
-                    const uint64_t w = clock - a4[j];
-                    const bool res = (sb & RS_RES) != 0;
-                    // exact without K1: FCFS (key 0, order = id) or P = S_c (w = 0 / zero rate)
-                    const bool trivial = !prio || w == 0 || sm.kc[c].zero;
-                    bool queue = false, enter = false;
-                    uint64_t key = 0;
-                    if (trivial) {
-                        if (prio) {
-                            const double S = sm.dS[c];
-                            key = (uint64_t)__double_as_longlong(S < kEps ? kEps : S);
+                    if (lean) {
+                        // skip when the exact cap or the FP32 bound proves rank after (kk, ki)
+                        // (a partial always gets its exact key on the first pass: R6 may need it)
+                        const bool part = first_pass && (sb & RS_RES);
+                        bool need = valid && (part || (!((skipm >> c) & 1u) && !(((tiem >> c) & 1u) && (uint32_t)e > ki)));
+                        const uint64_t w = clock - a4[j];
+                        if (need && w != 0 && !((zero_mask >> c) & 1u) && !part) {
+                            const float pf = k1_filter_f32(sm.kp.fS[c], sm.kp.fp2[c], sm.kp.fC2[c], w);
+                            need = !(__fadd_ru(pf, 1e-4f) < thrf);
                         }
-                        if (valid && first_pass && res) {
+                        qbits |= need ? (1u << j) : 0u;
+                    } else if (!prio) {
+                        // FCFS: every key is 0, the order is the id order (R4)
+                        any_direct |= valid && !(has_th && (uint32_t)e <= thi) && (uint32_t)e < ki;
+                        if (valid && first_pass && (sb & RS_RES)) {
                             const int slot = atomicAdd(&sm.npart, 1);
                             if (slot < kMaxPart) {
                                 sm.part[slot] = (uint32_t)e;
-                                sm.partkey[slot] = key;
+                                sm.partkey[slot] = 0;
                             }
                         }
-                        enter = valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
-                                before(key, (uint32_t)e, kk, ki);
-                    } else if (valid) {
-                        queue = true;
-                        if (filter_ok && !(first_pass && res)) {
-                            const float pf = k1_filter_f32(sm.fS[c], sm.fp2[c], sm.fC2[c], w);
-                            const double U = fmax(fmin((double)pf + kFilterDelta, sm.dSmax[c]), kEps);
-                            const bool can_enter = !(U < Pkk || (U == Pkk && (uint32_t)e > ki));
-                            bool excluded = false;
-                            if (has_th) {
-                                const double Lb = fmax(fmax((double)pf - kFilterDelta, sm.dS[c]), kEps);
-                                excluded = Lb > Pth || (Lb == Pth && (uint32_t)e < thi);
-                            }
-                            queue = can_enter && !excluded;
-                        }
+                    } else {
+                        qbits |= valid ? (1u << j) : 0u;     // exact key for every pending request
                     }
-                    take(key, (uint32_t)e, enter);
-                    const uint32_t qm = __ballot_sync(0xFFFFFFFFu, queue);
-                    if (queue) {
-                        const int pos = qn + __popc(qm & ((1u << lane) - 1));
-                        qid[pos] = (uint32_t)e;
-                        qw[pos] = w;
-                        qc[pos] = (uint8_t)(c | (res ? RS_RES : 0));
-                    }
-                    qn += __popc(qm);
                 }
-                __syncwarp();
-                while (qn >= 32) {
-                    refine(32);
-                    uint32_t tid4[4];
-                    uint64_t tw4[4];
-                    uint8_t tc4[4];
+                if (!prio && __any_sync(0xFFFFFFFFu, any_direct)) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {                 // qn - 32 <= 128 left to shift
-                        const int q = 32 + lane + 32 * k;
-                        if (q < qn) {
-                            tid4[k] = qid[q];
-                            tw4[k] = qw[q];
-                            tc4[k] = qc[q];
+                    for (int j = 0; j < 4; ++j) {
+                        const int e = e0 + j;
+                        const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
+                        const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
+                        take(0, (uint32_t)e, valid && !(has_th && (uint32_t)e <= thi) && before(0, (uint32_t)e, kk, ki));
+                    }
+                }
+                if (__any_sync(0xFFFFFFFFu, qbits != 0)) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const bool queue = (qbits >> j) & 1u;
+                        const uint32_t qm = __ballot_sync(0xFFFFFFFFu, queue);
+                        if (queue) {
+                            const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
+                            const int pos = qn + __popc(qm & ((1u << lane) - 1));
+                            qid[pos] = (uint32_t)(e0 + j);
+                            qw[pos] = clock - a4[j];
+                            qc[pos] = (uint8_t)((sb & RS_CLS) | (sb & RS_RES));
                         }
+                        qn += __popc(qm);
                     }
                     __syncwarp();
+                    while (qn >= 32) {
+                        refine(32);
+                        uint32_t tid4[4];
+                        uint64_t tw4[4];
+                        uint8_t tc4[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int q = 32 + lane + 32 * k;
-                        if (q < qn) {
-                            qid[q - 32] = tid4[k];
-                            qw[q - 32] = tw4[k];
-                            qc[q - 32] = tc4[k];
+                        for (int k = 0; k < 4; ++k) {             // qn - 32 <= 128 left to shift
+                            const int q = 32 + lane + 32 * k;
+                            if (q < qn) {
+                                tid4[k] = qid[q];
+                                tw4[k] = qw[q];
+                                tc4[k] = qc[q];
+                            }
                         }
+                        __syncwarp();
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int q = 32 + lane + 32 * k;
+                            if (q < qn) {
+                                qid[q - 32] = tid4[k];
+                                qw[q - 32] = tw4[k];
+                                qc[q - 32] = tc4[k];
+                            }
+                        }
+                        qn -= 32;
+                        __syncwarp();
                     }
-                    qn -= 32;
-                    __syncwarp();
                 }
             }
             if (qn > 0) refine(qn);
