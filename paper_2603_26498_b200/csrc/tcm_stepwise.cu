@@ -331,15 +331,39 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             uint64_t* qw = sm.qw[wg];
             uint8_t* qc = sm.qc[wg];
             auto take = [&](uint64_t key, uint32_t id, bool enter) {   // warp-collective
-                if (__any_sync(0xFFFFFFFFu, enter)) {
+                const uint32_t em = __ballot_sync(0xFFFFFFFFu, enter);
+                if (em == 0) return;
+                if (__popc(em) <= 6) {
+                    // few entrants: insert each into the sorted list (rank by ballot, shift by shuffle)
+                    uint32_t rest = em;
+                    while (rest) {
+                        const int src = __ffs(rest) - 1;
+                        rest &= rest - 1;
+                        const uint64_t xk = __shfl_sync(0xFFFFFFFFu, key, src);
+                        const uint32_t xi = __shfl_sync(0xFFFFFFFFu, id, src);
+                        if (!before(xk, xi, kk, ki)) continue;          // pushed out by an earlier insert
+                        const int pos = __popc(__ballot_sync(0xFFFFFFFFu, before(lk, li, xk, xi)));
+                        const uint64_t uk = __shfl_up_sync(0xFFFFFFFFu, lk, 1);
+                        const uint32_t ui = __shfl_up_sync(0xFFFFFFFFu, li, 1);
+                        if (lane > pos) {
+                            lk = uk;
+                            li = ui;
+                        } else if (lane == pos) {
+                            lk = xk;
+                            li = xi;
+                        }
+                        kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
+                        ki = __shfl_sync(0xFFFFFFFFu, li, 31);
+                    }
+                } else {
                     uint64_t bk = enter ? key : 0;
                     uint32_t bi = enter ? id : NIL;
                     warp_sort_desc(bk, bi, lane);
                     warp_merge(lk, li, bk, bi, lane);
                     kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
                     ki = __shfl_sync(0xFFFFFFFFu, li, 31);
-                    retune();
                 }
+                retune();
             };
             auto refine = [&](int cnt) {                               // exact keys for <= 32 queued
                 uint64_t key = 0;

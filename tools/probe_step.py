@@ -17,7 +17,7 @@ def stage(R, pending, engine):
     sim.load(tr, res)
     return sim, res
 
-CONFIGS = [(65536, 1024), (8192, 1024), (1, 100000)]
+CONFIGS = [(65536, 1024), (16384, 4096), (4096, 16384), (1, 100000)]
 ENGINES = (tcm.ENGINE_STEPWISE, tcm.ENGINE_FUSED)
 if len(sys.argv) > 2:
     CONFIGS = [(int(sys.argv[1]), int(sys.argv[2]))]
