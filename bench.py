@@ -292,7 +292,9 @@ def run_tcm(args, rank, world, local):
     log(f"timed: {ms:.1f} ms for {args.steps} steps")
     # stepwise (paper-literal) per-step kernel on C2': its own HBM roofline
     if not args.skip_step and rank == 0:
-        out["roofline_step"] = bench_stepwise(args, dev, stream)
+        st_res = bench_stepwise(args, dev, stream)
+        out["roofline_step"] = st_res.pop("C2'")
+        out["step_kernels"] = st_res
 
     # end-to-end through the C ABI with HOST buffers (H2D + run + D2H inside the timed region)
     log("stepwise done")
@@ -313,14 +315,11 @@ def run_tcm(args, rank, world, local):
         print(json.dumps(out), flush=True)
 
 
-def bench_stepwise(args, dev, stream):
-    """One paper-literal step (a1-a5) over C2': 65,536 replicas x ~1k pending."""
+def _stage_c2(replicas, pending, engine, dev, stream):
     import torch
-    import tracegen as T
     from paper_2603_26498_b200 import tcm
     from paper_2603_26498_b200 import workloads as W
-
-    sw = W.c2prime(replicas=args.step_replicas, pending=args.step_pending)
+    sw = W.c2prime(replicas=replicas, pending=pending)
     with torch.cuda.stream(stream):
         tr = tcm.generate_device(sw.gen, device=dev, stream=stream)
         first = tr["req_offset"][:-1].to(torch.int64)
@@ -329,13 +328,19 @@ def bench_stepwise(args, dev, stream):
         tr["footprint"].view(torch.int32)[first] = 800
         tr["params"] = torch.from_numpy(sw.params.view(np.uint8)).to(dev)
     stream.synchronize()
-    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE), stream)
+    sim = tcm.Simulation(tcm.config(engine=engine), stream)
     sim.load(tr, None)
+    return sim
+
+
+def time_steps(sim, stream, iters, reps):
+    """Device time of single engine iterations 2..iters+1 (iteration 1 runs request 0 alone)."""
+    import torch
     times, pend = [], []
-    for rep in range(args.step_reps):
+    for rep in range(reps):
         sim.reset()
-        sim.step(1)                 # iteration 1: request 0 alone (60 s inline)
-        for it in range(args.step_iters):
+        sim.step(1)
+        for _ in range(iters):
             s0 = sim.stats()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -347,23 +352,46 @@ def bench_stepwise(args, dev, stream):
             if rep > 0:            # first repetition is warm-up
                 times.append(e0.elapsed_time(e1))
                 pend.append(s1["sum_pending"] - s0["sum_pending"])
-    sim.close()
+    return float(np.mean(times)), float(np.mean(pend))
+
+
+def bench_stepwise(args, dev, stream):
+    """Paper-literal per-step kernel (k_step: a1-a5, every pending request re-keyed) on C2'
+     and on a larger-window variant; the fused engine's time for the same
+    iteration alongside."""
+    from paper_2603_26498_b200 import tcm
     peak, peak_kind = peak_hbm()
-    ms = float(np.mean(times))
-    bytes_per = float(np.mean(pend)) * STEP_BYTES_PER_PENDING + args.step_replicas * STEP_BYTES_PER_DECISION
-    achieved = bytes_per / (ms / 1e3) / 1e9
-    traffic = None
+    out = {}
+    for name, R, P in (("C2'", args.step_replicas, args.step_pending), ("C2'-wide", args.step_replicas // 4, args.step_pending * 4)):
+        sim = _stage_c2(R, P, tcm.ENGINE_STEPWISE, dev, stream)
+        ms, keys = time_steps(sim, stream, args.step_iters, args.step_reps)
+        sim.close()
+        fsim = _stage_c2(R, P, tcm.ENGINE_FUSED, dev, stream)
+        fms, _ = time_steps(fsim, stream, args.step_iters, 2)
+        fsim.close()
+        bytes_per = keys * STEP_BYTES_PER_PENDING + R * STEP_BYTES_PER_DECISION
+        achieved = bytes_per / (ms / 1e3) / 1e9
+        out[name] = {"kernel": "k_step", "workload": f"{name}: {R} replicas x {P} pending, one iteration (a1-a5)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "ms_per_step": ms, "keys_per_step": keys,
+                     "keys_per_s": keys / (ms / 1e3), "decisions_per_s": R / (ms / 1e3),
+                     "fused_engine_ms_per_step": fms}
     prof = os.path.join(ROOT, "profiles", "step_dram_bytes.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            out["C2'"]["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
-    return {"kernel": "k_step", "workload": f"C2': {args.step_replicas} replicas x {args.step_pending} pending, "
-            "one iteration (a1-a5), stepwise engine", "bound": "hbm", "achieved": achieved, "peak": peak,
-            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-            "ms_per_step": ms, "keys_per_step": float(np.mean(pend)),
-            "decisions_per_s": args.step_replicas / (ms / 1e3)}
+            pass
+    # C2: one queue with 100k pending requests, per-step latency (BASELINE.json configs[1])
+    lat = {}
+    for eng, nm in ((tcm.ENGINE_STEPWISE, "stepwise"), (tcm.ENGINE_FUSED, "fused")):
+        sim = _stage_c2(1, 100_000, eng, dev, stream)
+        ms, keys = time_steps(sim, stream, args.step_iters, args.step_reps)
+        sim.close()
+        lat[nm + "_us"] = ms * 1e3
+    lat["pending"] = keys
+    out["C2_latency"] = lat
+    return out
 
 
 def bench_e2e(args, sw, trace, dev, stream, dist, world):
