@@ -101,7 +101,7 @@ def lib():
                                   ctypes.c_uint32, ctypes.c_uint16]
         L.orc_simulate.restype = i
         L.orc_simulate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32] + \
-            [ctypes.c_void_p] * 10 + [ctypes.c_void_p, u64, ctypes.c_void_p]
+            [ctypes.c_void_p] * 10 + [ctypes.c_void_p, u64, ctypes.c_void_p, u64]
         L.orc_ttft_bucket.restype = ctypes.c_uint32
         L.orc_ttft_bucket.argtypes = [u64]
         L.orc_aggregate.restype = None
@@ -186,7 +186,7 @@ class Result:
 
 def simulate(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM, alpha=1.0,
              kv_capacity=131072, chunk_budget=2048, m: OrcModel | None = None,
-             log: bool = False) -> Result:
+             log: bool = False, max_iters: int = 0) -> Result:
     """Run one replica through the oracle engine loop."""
     m = m or model()
     a = np.ascontiguousarray(arrival_us, dtype=np.uint64)
@@ -211,7 +211,7 @@ def simulate(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM,
         ctypes.byref(m), ctypes.byref(r), n, a.ctypes.data, f.ctypes.data, il.ctypes.data,
         o.ctypes.data, md.ctypes.data, seq.ctypes.data, ft.ctypes.data, dn.ctypes.data,
         cl.ctypes.data, ctypes.byref(cnt), None if logbuf is None else logbuf.ctypes.data, cap,
-        ctypes.byref(log_n))
+        ctypes.byref(log_n), max_iters)
     counters = {name: getattr(cnt, name) for name, _ in OrcCounters._fields_}
     iters = None
     if log:
@@ -221,11 +221,11 @@ def simulate(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM,
 
 
 def simulate_trace(tr, r: int, policy=TCM, alpha=1.0, kv_capacity=131072, chunk_budget=2048,
-                   m=None, log=False) -> Result:
+                   m=None, log=False, max_iters=0) -> Result:
     a, b = int(tr.offset[r]), int(tr.offset[r + 1])
     return simulate(tr.arrival_us[a:b], tr.footprint[a:b], tr.inline_us[a:b],
                     tr.out_tokens[a:b], tr.modality[a:b], policy, alpha, kv_capacity,
-                    chunk_budget, m, log)
+                    chunk_budget, m, log, max_iters)
 
 
 def aggregate(tr_slice, res: Result, chunk_budget=2048, m=None, hist=None, cnt=None):

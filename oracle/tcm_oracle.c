@@ -164,7 +164,8 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
                  const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
                  const uint16_t* out, const uint8_t* mod, uint32_t* admit_seq,
                  uint64_t* first_token, uint64_t* done, uint8_t* cls_out,
-                 orc_counters* cnt, orc_iter_rec* log, uint64_t log_cap, uint64_t* log_n)
+                 orc_counters* cnt, orc_iter_rec* log, uint64_t log_cap, uint64_t* log_n,
+                 uint64_t max_iters)
 {
     memset(cnt, 0, sizeof(*cnt));
     if (log_n) *log_n = 0;
@@ -194,6 +195,7 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
     int status = 0;
 
     for (;;) {
+        if (max_iters && iter >= max_iters) break;   /* truncated run (test infrastructure) */
         /* 1 ingest arrivals <= clock, classify on ingest */
         while (nxt < n && arrival[nxt] <= clock) {
             cls_out[nxt] = (uint8_t)orc_classify(m, mod[nxt], f[nxt]);

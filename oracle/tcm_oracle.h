@@ -87,7 +87,9 @@ uint64_t orc_iso_e2e(const orc_model* m, uint32_t chunk_budget, uint32_t footpri
  * Simulate one replica to completion (SURVEY.md 8(c) pseudo-code, steps 1-10).
  * Inputs: n requests sorted by (arrival, id).  Outputs (per request): admit_seq,
  * first_token_us, done_us, cls.  iter_log may be NULL; otherwise it receives up to
- * log_cap records and *log_n is set to the number of iterations.
+ * log_cap records and *log_n is set to the number of iterations.  max_iters > 0 stops the
+ * run after that many engine iterations (for comparing the first steps of huge queues);
+ * unfinished requests then keep admit_seq / first_token / done as initialised by the caller.
  * Returns 0, or -1 (argument/capacity error), -2 (deadlock: unreachable under R6).
  */
 int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
@@ -96,7 +98,8 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
                  const uint8_t* modality,
                  uint32_t* admit_seq, uint64_t* first_token_us, uint64_t* done_us,
                  uint8_t* cls_out, orc_counters* cnt,
-                 orc_iter_rec* iter_log, uint64_t log_cap, uint64_t* log_n);
+                 orc_iter_rec* iter_log, uint64_t log_cap, uint64_t* log_n,
+                 uint64_t max_iters);
 
 /* ---- a6 aggregation: HDR-style TTFT bucket and per-group counters ---- */
 enum { ORC_HIST_BINS = 496, ORC_GROUPS = 4, ORC_NCNT = 6 };
