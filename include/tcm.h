@@ -133,6 +133,8 @@ typedef struct tcm_stats_host {
     uint64_t replicas_done;
     uint64_t replicas_active;
     uint64_t kernel_launches;  /* library kernels launched since tcm_create          */
+    uint64_t scanned_decisions; /* decisions that ran the full key/order/scan (the rest
+                                   were taken in closed form, Lemma L4)  */
     int32_t first_bad_replica; /* -1 if none                                          */
     int32_t first_bad_status;
 } tcm_stats_host;

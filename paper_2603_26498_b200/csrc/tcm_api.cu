@@ -376,6 +376,7 @@ tcm_status tcm_stats(tcm_ctx* c, tcm_stats_host* out, int64_t* dev_hist, int64_t
         out->requests_done = h[kAccDone];
         out->replicas_done = h[kAccReplicasDone];
         out->replicas_active = h[kAccReplicasActive];
+        out->scanned_decisions = h[kAccScanned];
         out->first_bad_replica = h[kAccBadStatus] ? (int32_t)h[kAccBadReplica] : -1;
         out->first_bad_status = (int32_t)h[kAccBadStatus];
     }

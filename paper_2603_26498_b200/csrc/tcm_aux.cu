@@ -33,7 +33,7 @@ __global__ void k_init(TraceDev t) {
     st.ff_iters = 0;
     st.idle_jumps = 0;
     st.done_count = 0;
-    st.pad = 0;
+    st.scanned = 0;
     t.state[r] = st;
 }
 
@@ -119,7 +119,7 @@ __global__ void k_reduce(TraceDev t, unsigned long long* acc /* [kAccN] */) {
         v[5] = st.done_count;
         v[6] = (st.flags & FLAG_FINISHED) ? 1 : 0;
         v[7] = (st.flags & FLAG_FINISHED) ? 0 : 1;
-        v[8] = 0;
+        v[8] = st.scanned;
         mx = st.max_pending;
         if (st.status != ST_OK) {
             atomicMin(reinterpret_cast<unsigned long long*>(&acc[kAccBadReplica]), (unsigned long long)r);
@@ -127,12 +127,13 @@ __global__ void k_reduce(TraceDev t, unsigned long long* acc /* [kAccN] */) {
         }
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = warp_sum64(v[k]);
+    for (int k = 0; k < 9; ++k) v[k] = warp_sum64(v[k]);
     mx = __reduce_max_sync(0xFFFFFFFFu, mx);
     if ((threadIdx.x & 31) == 0) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (v[k]) atomicAdd(&acc[k], (unsigned long long)v[k]);
+        if (v[8]) atomicAdd(&acc[kAccScanned], (unsigned long long)v[8]);
         atomicMax(&acc[kAccMaxPending], (unsigned long long)mx);
     }
 }
@@ -146,58 +147,76 @@ __device__ __forceinline__ uint32_t ttft_bucket(uint64_t t) {
     return 16u + 8u * (e - 4u) + (uint32_t)((t >> (e - 3u)) & 7u);
 }
 
-__global__ void k_aggregate(ModelConst m, TraceDev t, unsigned long long* hist, unsigned long long* cnt) {
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// A block aggregates a tile of kAggTile consecutive replicas: histogram bins are counted in a
+// shared-memory copy for the tile's (first) cell and flushed once; replicas of another cell in the
+// same tile (cell boundaries) fall back to global atomics.  Counters are warp-reduced per replica.
+constexpr uint32_t kAggTile = 32;
+
+__global__ void __launch_bounds__(256) k_aggregate(ModelConst m, TraceDev t, unsigned long long* hist,
+                                                   unsigned long long* cnt) {
+    __shared__ unsigned long long sh[kGroups * kHistBins];
+    const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    if (warp >= t.R) return;
-    const uint32_t r = warp;
-    const tcm_replica_params p = t.params[r];
-    const uint64_t a = t.offset[r], b = t.offset[r + 1];
-    const uint64_t B = p.chunk_budget;
-    uint64_t c[3][kNcnt];
+    const uint32_t r0 = blockIdx.x * kAggTile;
+    if (r0 >= t.R) return;
+    const uint32_t r1 = r0 + kAggTile < t.R ? r0 + kAggTile : t.R;
+    const uint32_t cell0 = t.params[r0].cell_id;
+    for (uint32_t i = threadIdx.x; i < kGroups * kHistBins; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (uint32_t r = r0 + warp; r < r1; r += blockDim.x / 32) {
+        const tcm_replica_params p = t.params[r];
+        const uint64_t a = t.offset[r], b = t.offset[r + 1];
+        const uint64_t B = p.chunk_budget;
+        const bool local = p.cell_id == cell0;
+        unsigned long long* H = local ? sh : hist + (size_t)p.cell_id * kGroups * kHistBins;
+        uint64_t c[3][kNcnt];
 #pragma unroll
-    for (int g = 0; g < 3; ++g)
+        for (int g = 0; g < 3; ++g)
 #pragma unroll
-        for (int k = 0; k < (int)kNcnt; ++k) c[g][k] = 0;
-    unsigned long long* H = hist + (size_t)p.cell_id * kGroups * kHistBins;
-    for (uint64_t i = a + lane; i < b; i += 32) {
-        const uint32_t f = t.footprint[i];
-        const uint32_t o = t.out[i];
-        const int g = classify(m, t.mod[i], f);
-        const uint64_t arr = t.arrival[i];
-        const uint64_t ttft = t.first_token[i] - arr;
-        const uint64_t e2e = t.done[i] - arr;
-        const uint64_t iso = (uint64_t)t.inl[i] + ((uint64_t)f + B - 1) / B * m.c0 + m.cp * f +
-                             (uint64_t)(o - 1) * (m.c0 + m.cd);
-        const uint64_t lhs = e2e * m.slo_den, rhs = iso * m.slo_num;
-        const bool viol = lhs > rhs;
-        const uint32_t bk = ttft_bucket(ttft);
-        atomicAdd(&H[(size_t)g * kHistBins + bk], 1ull);
-        atomicAdd(&H[(size_t)3 * kHistBins + bk], 1ull);
+            for (int k = 0; k < (int)kNcnt; ++k) c[g][k] = 0;
+        for (uint64_t i = a + lane; i < b; i += 32) {
+            const uint32_t f = t.footprint[i];
+            const uint32_t o = t.out[i];
+            const int g = classify(m, t.mod[i], f);
+            const uint64_t arr = t.arrival[i];
+            const uint64_t ttft = t.first_token[i] - arr;
+            const uint64_t e2e = t.done[i] - arr;
+            const uint64_t iso = (uint64_t)t.inl[i] + ((uint64_t)f + B - 1) / B * m.c0 + m.cp * f +
+                                 (uint64_t)(o - 1) * (m.c0 + m.cd);
+            const uint64_t lhs = e2e * m.slo_den, rhs = iso * m.slo_num;
+            const bool viol = lhs > rhs;
+            const uint32_t bk = ttft_bucket(ttft);
+            atomicAdd(&H[(size_t)g * kHistBins + bk], 1ull);
+            atomicAdd(&H[(size_t)3 * kHistBins + bk], 1ull);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            if (q == g) {
-                c[q][0] += 1;
-                c[q][1] += ttft;
-                c[q][2] += e2e;
-                c[q][3] += viol ? 1 : 0;
-                c[q][4] += viol ? lhs - rhs : 0;
-                c[q][5] += e2e / o;
+            for (int q = 0; q < 3; ++q) {
+                if (q == g) {
+                    c[q][0] += 1;
+                    c[q][1] += ttft;
+                    c[q][2] += e2e;
+                    c[q][3] += viol ? 1 : 0;
+                    c[q][4] += viol ? lhs - rhs : 0;
+                    c[q][5] += e2e / o;
+                }
             }
         }
-    }
-    unsigned long long* C = cnt + (size_t)p.cell_id * kGroups * kNcnt;
+        unsigned long long* C = cnt + (size_t)p.cell_id * kGroups * kNcnt;
 #pragma unroll
-    for (int k = 0; k < (int)kNcnt; ++k) {
-        uint64_t all = 0;
+        for (int k = 0; k < (int)kNcnt; ++k) {
+            uint64_t all = 0;
 #pragma unroll
-        for (int g = 0; g < 3; ++g) {
-            const uint64_t s = warp_sum64(c[g][k]);
-            all += s;
-            if (lane == 0 && s) atomicAdd(&C[g * kNcnt + k], (unsigned long long)s);
+            for (int g = 0; g < 3; ++g) {
+                const uint64_t s = warp_sum64(c[g][k]);
+                all += s;
+                if (lane == 0 && s) atomicAdd(&C[g * kNcnt + k], (unsigned long long)s);
+            }
+            if (lane == 0 && all) atomicAdd(&C[3 * kNcnt + k], (unsigned long long)all);
         }
-        if (lane == 0 && all) atomicAdd(&C[3 * kNcnt + k], (unsigned long long)all);
     }
+    __syncthreads();
+    unsigned long long* H0 = hist + (size_t)cell0 * kGroups * kHistBins;
+    for (uint32_t i = threadIdx.x; i < kGroups * kHistBins; i += blockDim.x)
+        if (sh[i]) atomicAdd(&H0[i], sh[i]);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -313,8 +332,7 @@ void launch_reduce(const TraceDev& t, unsigned long long* acc, cudaStream_t s) {
 }
 void launch_aggregate(const ModelConst& m, const TraceDev& t, unsigned long long* hist,
                       unsigned long long* cnt, cudaStream_t s) {
-    const uint64_t threads = (uint64_t)t.R * 32;
-    k_aggregate<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(m, t, hist, cnt);
+    k_aggregate<<<(t.R + kAggTile - 1) / kAggTile, 256, 0, s>>>(m, t, hist, cnt);
 }
 void launch_generate(const void* reps, uint32_t R, const uint64_t* off, uint64_t* arrival,
                      uint32_t* footprint, uint32_t* inl, uint16_t* out, uint8_t* mod, uint32_t* bad,

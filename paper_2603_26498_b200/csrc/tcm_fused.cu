@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
         st.clock += m.c0 + m.cp * tok + m.cd * (uint64_t)st.n_dec + inl_sum;
         st.iter++;
         st.decisions++;
+        st.scanned++;
         st.sum_pending += st.n_pend;
         st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
         budget--;

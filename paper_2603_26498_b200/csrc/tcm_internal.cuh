@@ -38,7 +38,7 @@ struct __align__(16) ReplicaState {
     uint64_t ff_iters;
     uint64_t idle_jumps;
     uint32_t done_count;
-    uint32_t pad;
+    uint32_t scanned;        // decisions that ran the full key/merge/scan (not fast-forwarded)
 };
 static_assert(sizeof(ReplicaState) == 128, "ReplicaState must be one 128-byte line");
 

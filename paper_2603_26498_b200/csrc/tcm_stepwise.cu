@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 st.iter++;
                 st.head[1]--;
                 st.decisions++;
+                st.scanned++;
                 st.sum_pending += st.n_pend;
                 st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
                 const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};

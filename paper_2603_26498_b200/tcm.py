@@ -66,7 +66,7 @@ class tcm_results_view(ctypes.Structure):
 class tcm_stats_host(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "iterations", "decisions", "ff_iterations", "idle_jumps", "sum_pending", "max_pending",
-        "requests_done", "replicas_done", "replicas_active", "kernel_launches")] + [
+        "requests_done", "replicas_done", "replicas_active", "kernel_launches", "scanned_decisions")] + [
         ("first_bad_replica", ctypes.c_int32), ("first_bad_status", ctypes.c_int32)]
 
 
