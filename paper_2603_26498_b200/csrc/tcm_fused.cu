@@ -91,16 +91,8 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
     const bool prio = prm.policy == TCM_POLICY_TCM;
     const uint32_t B = prm.chunk_budget;
     K1Class kc[3];
-    double cap[3];        // exact upper bound of P per class: fl(S_c + 1), or S_c at zero rate
-    uint64_t capk[3];     // its key bits
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        kc[c] = k1_class(m.S[c], m.k[c], m.p[c], prm.aging_alpha);
-        cap[c] = kc[c].zero ? kc[c].S : __dadd_rn(kc[c].S, 1.0);
-        capk[c] = (uint64_t)__double_as_longlong(cap[c] < kEps ? kEps : cap[c]);
-    }
-    int sat_c = -1;       // class whose head sat_id is known to have key == capk (L4b)
-    uint32_t sat_id = NIL;
+    for (int c = 0; c < 3; ++c) kc[c] = k1_class(m.S[c], m.k[c], m.p[c], prm.aging_alpha);
 
     // Register caches: each class queue's head (arrival, footprint) and its successor
     // (id, arrival, footprint) so that advancing a queue never waits on memory; the next
@@ -197,21 +189,6 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
             for (int c = 0; c < 3; ++c)
                 if (st.head[c] != NIL && (((st.flags >> c) & 1u) || (uint64_t)hf[c] <= st.kv_free)) stuck = false;
         }
-        // L4b: the top-ranked head is known to sit at its class cap (saturated key, which K1's
-        // monotonicity keeps there) and every other non-empty class has a strictly lower cap, so
-        // it stays on top; if it does not fit and nothing is partial, nothing can prefill.
-        if (!stuck && prio && sat_c >= 0 && (st.flags & 7u) == 0) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                if (c == sat_c && st.head[c] == sat_id && (uint64_t)hf[c] > st.kv_free) {
-                    bool dom = true;
-#pragma unroll
-                    for (int d = 0; d < 3; ++d)
-                        if (d != c && st.head[d] != NIL && !(cap[d] < cap[c])) dom = false;
-                    stuck = dom;
-                }
-            }
-        }
         if (stuck && st.n_dec > 0) {
             const uint64_t F = next_fin;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
@@ -251,18 +228,6 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
             csf[c] = sf[c];
             cres[c] = (st.flags >> c) & 1u;
             key[c] = (prio && cur[c] != NIL) ? k1_key(kc[c], st.clock - carr[c]) : 0;
-        }
-        if (prio) {                                         // remember a saturated head (L4b)
-            uint64_t best_cap = 0;
-            sat_c = -1;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                if (cur[c] != NIL && key[c] == capk[c] && capk[c] > best_cap) {
-                    best_cap = capk[c];
-                    sat_c = c;
-                    sat_id = cur[c];
-                }
-            }
         }
         while (left > 0) {
             int best = -1;
