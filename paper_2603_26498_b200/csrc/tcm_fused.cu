@@ -67,7 +67,7 @@ __device__ __forceinline__ uint64_t cal_next(const Cal& c, uint64_t iter) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t max_iters,
+__global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint32_t max_iters,
                                               uint32_t* active) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= t.R) return;
@@ -91,8 +91,17 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
     const bool prio = prm.policy == TCM_POLICY_TCM;
     const uint32_t B = prm.chunk_budget;
     K1Class kc[3];
+    float fS[3], fp2[3], fC2[3];
+    bool use_bound = true;     // FP32 bound validated for these constants
 #pragma unroll
-    for (int c = 0; c < 3; ++c) kc[c] = k1_class(m.S[c], m.k[c], m.p[c], prm.aging_alpha);
+    for (int c = 0; c < 3; ++c) {
+        kc[c] = k1_class(m.S[c], m.k[c], m.p[c], prm.aging_alpha);
+        const double c2 = __dmul_rn(kc[c].C, 1.4426950408889634);
+        fS[c] = (float)kc[c].S;
+        fp2[c] = (float)kc[c].p;
+        fC2[c] = (float)c2;
+        if (!kc[c].zero && !(kc[c].p <= 16.0 && fabs(c2) <= 1000.0)) use_bound = false;
+    }
 
     // Register caches: each class queue's head (arrival, footprint) and its successor
     // (id, arrival, footprint) so that advancing a queue never waits on memory; the next
@@ -216,7 +225,13 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
         bool blocked = false;                               // R6
         uint32_t cur[3], crem[3], cf[3], csid[3], csf[3];
         uint64_t carr[3], key[3], csarr[3];
-        bool cres[3];
+        float pf[3];          // FP32 bound of each head's priority (|P~ - P| <= 1e-5)
+        bool cres[3], ex[3];  // ex[c]: key[c] holds the exact K1 key
+        // Two heads whose bounds are more than 2.5e-4 apart are ordered by the bounds (the exact
+        // order, since the bound error is < 1e-5); only closer pairs get their exact FP64 keys.
+        auto bound = [&](int c, uint64_t w) -> float {
+            return (w == 0 || kc[c].zero || !use_bound) ? (float)kc[c].S : k1_filter_f32(fS[c], fp2[c], fC2[c], w);
+        };
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             cur[c] = st.head[c];
@@ -227,20 +242,50 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
             csarr[c] = sarr[c];
             csf[c] = sf[c];
             cres[c] = (st.flags >> c) & 1u;
-            key[c] = (prio && cur[c] != NIL) ? k1_key(kc[c], st.clock - carr[c]) : 0;
+            key[c] = 0;
+            ex[c] = !prio;
+            pf[c] = (prio && cur[c] != NIL) ? bound(c, st.clock - carr[c]) : 0.0f;
         }
         while (left > 0) {
             int best = -1;
             uint64_t bk = 0, ba = 0;
             uint32_t bi = 0;
+            float bpf = 0.0f;
+            bool bex = true;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (cur[c] != NIL && (!blocked || cres[c])) {
-                    const bool better = best < 0 || key[c] > bk ||
-                                        (key[c] == bk && (carr[c] < ba || (carr[c] == ba && cur[c] < bi)));
+                    bool better = best < 0;
+                    if (!better) {
+                        const float d = pf[c] - bpf;
+                        if (use_bound && d > 2.5e-4f) {
+                            better = true;
+                        } else if (use_bound && d < -2.5e-4f) {
+                            better = false;
+                        } else {
+                            if (!ex[c]) {
+                                key[c] = k1_key(kc[c], st.clock - carr[c]);
+                                ex[c] = true;
+                            }
+                            if (!bex) {
+#pragma unroll
+                                for (int q = 0; q < c; ++q) {
+                                    if (q == best) {
+                                        key[q] = k1_key(kc[q], st.clock - carr[q]);
+                                        ex[q] = true;
+                                        bk = key[q];
+                                    }
+                                }
+                                bex = true;
+                            }
+                            better = key[c] > bk || (key[c] == bk && (carr[c] < ba || (carr[c] == ba && cur[c] < bi)));
+                        }
+                    }
                     if (better) {
                         best = c;
                         bk = key[c];
+                        bex = ex[c];
+                        bpf = pf[c];
                         ba = carr[c];
                         bi = cur[c];
                     }
@@ -279,7 +324,8 @@ __global__ void __launch_bounds__(64) k_fused(ModelConst m, TraceDev t, uint32_t
                                 cf[c] = csf[c];
                                 crem[c] = cf[c];
                                 cres[c] = false;
-                                if (prio) key[c] = k1_key(kc[c], st.clock - carr[c]);
+                                ex[c] = !prio;
+                                if (prio) pf[c] = bound(c, st.clock - carr[c]);
                                 csid[c] = ni != st.tail[c] ? link[ni] : NIL;
                                 csarr[c] = csid[c] != NIL ? arr[csid[c]] : 0;
                                 csf[c] = csid[c] != NIL ? fp[csid[c]] : 0;
