@@ -34,6 +34,22 @@ constexpr uint32_t ST_PARTIAL_OVERFLOW = 4;
 // request-state byte
 constexpr uint8_t RS_CLS = 3, RS_PEND = 4, RS_RES = 8, RS_FT = 16;
 
+// stream staging: per warp, kStages chunks of 128 requests (1 KB arrivals + 128 B states)
+constexpr int kStages = 3;
+constexpr size_t kRingBytes = (size_t)kWarpsPerBlock * kStages * (128 * 8 + 32 * 4);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ bool before(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
     return ka > kb || (ka == kb && ia < ib);
 }
@@ -242,6 +258,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
     constexpr int kMaxDone = GroupSmem<G>::kMaxDone;
     __shared__ double s_lnR[16], s_lnT[16], s_expT[16];
     __shared__ GroupSmem<G> smg[kGroups];
+    extern __shared__ __align__(16) uint8_t dsm[];
+    uint64_t* ring_a = reinterpret_cast<uint64_t*>(dsm);
+    uint32_t* ring_s = reinterpret_cast<uint32_t*>(dsm + (size_t)kWarpsPerBlock * kStages * 128 * 8);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int group = warp / G, wg = warp % G;       // warp index inside the group
     GroupSmem<G>& sm = smg[group];
@@ -389,34 +408,38 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             const bool lean = prio && filter_ok && !has_th;    // FP32-bound path (else: exact for all)
             const int64_t gstart = (int64_t)((base + lo) & ~3ull) - (int64_t)base;   // 4-aligned globally
             const int64_t stride = (int64_t)G * 128;
-            auto load4 = [&](int64_t e0, uint64_t (&a4)[4], uint32_t& s4) {
-                s4 = 0;
-                if (e0 >= 0 && e0 + 3 < (int64_t)hi) {
-                    const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(arr + e0));
-                    const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(arr + e0 + 2));
-                    a4[0] = v0.x;
-                    a4[1] = v0.y;
-                    a4[2] = v1.x;
-                    a4[3] = v1.y;
-                    s4 = *reinterpret_cast<const uint32_t*>(rsc + e0);
-                } else {
+            // cp.async ring: kStages chunks of 128 requests per warp in flight; lane l copies and
+            // later consumes exactly its own 4 requests (32 B of arrivals + 4 state bytes), so
+            // no cross-lane barrier is needed, only cp.async.wait_group.
+            uint64_t* ra = ring_a + (size_t)warp * kStages * 128;
+            uint32_t* rst = ring_s + (size_t)warp * kStages * 32;
+            auto issue = [&](int64_t g, int slot) {
+                const int64_t e0 = g + 4 * lane;
+                if (g < (int64_t)hi) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int64_t e = e0 + j;
-                        const bool ok = e >= (int64_t)lo && e < (int64_t)hi;
-                        a4[j] = ok ? arr[e] : 0;
-                        s4 |= (uint32_t)(ok ? rsc[e] : 0) << (8 * j);
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t e = e0 + 2 * h;
+                        int64_t nb = (int64_t)hi - e;
+                        nb = nb < 0 ? 0 : (nb > 2 ? 2 : nb);
+                        cp_async16(ra + slot * 128 + 4 * lane + 2 * h, nb ? arr + e : arr, (int)(8 * nb));
                     }
+                    int64_t ns = (int64_t)hi - e0;
+                    ns = ns < 0 ? 0 : (ns > 4 ? 4 : ns);
+                    cp_async4(rst + slot * 32 + lane, ns ? rsc + e0 : rsc, (int)ns);
                 }
+                cp_async_commit();
             };
             int64_t g0 = gstart + (int64_t)wg * 128;
-            uint64_t na4[4] = {0, 0, 0, 0};
-            uint32_t ns4 = 0;
-            if (g0 < (int64_t)hi) load4(g0 + 4 * lane, na4, ns4);
-            for (; g0 < (int64_t)hi; g0 += stride) {
-                const uint64_t a4[4] = {na4[0], na4[1], na4[2], na4[3]};
-                const uint32_t s4 = ns4;
-                if (g0 + stride < (int64_t)hi) load4(g0 + stride + 4 * lane, na4, ns4);   // prefetch
+#pragma unroll
+            for (int q = 0; q < kStages - 1; ++q) issue(g0 + q * stride, q);
+            for (int kchunk = 0; g0 < (int64_t)hi; g0 += stride, ++kchunk) {
+                issue(g0 + (kStages - 1) * stride, (kchunk + kStages - 1) % kStages);
+                cp_async_wait<kStages - 1>();
+                const int slot = kchunk % kStages;
+                const ulonglong2 v0 = *reinterpret_cast<const ulonglong2*>(ra + slot * 128 + 4 * lane);
+                const ulonglong2 v1 = *reinterpret_cast<const ulonglong2*>(ra + slot * 128 + 4 * lane + 2);
+                const uint64_t a4[4] = {v0.x, v0.y, v1.x, v1.y};
+                const uint32_t s4 = rst[slot * 32 + lane];
                 const int e0 = (int)(g0 + 4 * lane);
                 uint32_t qbits = 0;                       // bit j: element j goes to the refine queue
                 bool any_direct = false;
@@ -504,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     }
                 }
             }
+            cp_async_wait<0>();
             if (qn > 0) refine(qn);
             if (G > 1) {
                 sm.wkey[wg][lane] = lk;
@@ -737,8 +761,10 @@ Launch stepwise_config(uint32_t R) {
     int dev = 0, sms = 148, per_sm1 = 1, per_sm8 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8>, kThreads, 0);
+    cudaFuncSetAttribute(k_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1>, kThreads, kRingBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8>, kThreads, kRingBytes);
     if (per_sm1 < 1) per_sm1 = 1;
     if (per_sm8 < 1) per_sm8 = 1;
     // Warp per replica when there are enough replicas to fill every warp slot twice over;
@@ -775,8 +801,8 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         if (cudaMemsetAsync(d_active, 0, 4, s) != cudaSuccess) return TCM_E_CUDA;
         for (uint32_t q = 0; q < this_chunk; ++q) {
             const int last = q + 1 == this_chunk;
-            if (L.group == 1) k_step<1><<<L.grid, kThreads, 0, s>>>(m, t, remv, d_active, last);
-            else k_step<8><<<L.grid, kThreads, 0, s>>>(m, t, remv, d_active, last);
+            if (L.group == 1) k_step<1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+            else k_step<8><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
             (*launches)++;
         }
         done_launches += this_chunk;
