@@ -267,6 +267,12 @@ def to_device(trace, params: np.ndarray, device="cuda") -> dict:
     return d
 
 
+def to_device_params(params: np.ndarray, device="cuda"):
+    """PARAMS_DTYPE records -> device byte tensor (tcm_replica_params[R])."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(params, dtype=PARAMS_DTYPE).view(np.uint8)).to(device)
+
+
 def alloc_results(n: int, device="cuda") -> dict:
     import torch
     return {"admit_seq": torch.empty(n, dtype=torch.uint32, device=device),
