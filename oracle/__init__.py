@@ -21,7 +21,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 
-FCFS, TCM = 0, 1
+FCFS, TCM, EDF, NAIVE_AGING = 0, 1, 2, 3
 HIST_BINS, GROUPS, NCNT = 496, 4, 6
 
 # Paper constants and SPEC cost model in integer us (R9).
@@ -46,6 +46,7 @@ class OrcReplica(ctypes.Structure):
     _fields_ = [
         ("policy", ctypes.c_uint32), ("chunk_budget", ctypes.c_uint32),
         ("kv_capacity", ctypes.c_uint64), ("alpha", ctypes.c_double),
+        ("admit_skip", ctypes.c_uint32), ("pad", ctypes.c_uint32),
     ]
 
 
@@ -186,7 +187,7 @@ class Result:
 
 def simulate(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM, alpha=1.0,
              kv_capacity=131072, chunk_budget=2048, m: OrcModel | None = None,
-             log: bool = False, max_iters: int = 0) -> Result:
+             log: bool = False, max_iters: int = 0, admit_skip: bool = False) -> Result:
     """Run one replica through the oracle engine loop."""
     m = m or model()
     a = np.ascontiguousarray(arrival_us, dtype=np.uint64)
@@ -200,7 +201,7 @@ def simulate(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM,
     dn = np.zeros(n, np.uint64)
     cl = np.zeros(n, np.uint8)
     cnt = OrcCounters()
-    r = OrcReplica(policy, chunk_budget, kv_capacity, alpha)
+    r = OrcReplica(policy, chunk_budget, kv_capacity, alpha, int(admit_skip), 0)
     cap = 0
     logbuf = None
     log_n = ctypes.c_uint64(0)
@@ -221,11 +222,11 @@ def simulate(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM,
 
 
 def simulate_trace(tr, r: int, policy=TCM, alpha=1.0, kv_capacity=131072, chunk_budget=2048,
-                   m=None, log=False, max_iters=0) -> Result:
+                   m=None, log=False, max_iters=0, admit_skip=False) -> Result:
     a, b = int(tr.offset[r]), int(tr.offset[r + 1])
     return simulate(tr.arrival_us[a:b], tr.footprint[a:b], tr.inline_us[a:b],
                     tr.out_tokens[a:b], tr.modality[a:b], policy, alpha, kv_capacity,
-                    chunk_budget, m, log, max_iters)
+                    chunk_budget, m, log, max_iters, admit_skip)
 
 
 def aggregate(tr_slice, res: Result, chunk_budget=2048, m=None, hist=None, cnt=None):

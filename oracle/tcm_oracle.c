@@ -145,6 +145,7 @@ uint64_t orc_iso_e2e(const orc_model* m, uint32_t B, uint32_t f, uint32_t inl, u
 typedef struct {
     double   P;
     uint64_t arrival;
+    uint64_t dl;        /* EDF: deadline x den = arrival*den + num*iso_e2e; aging: clock - arrival */
     uint32_t id;
 } orc_entry;
 
@@ -160,6 +161,26 @@ static int orc_cmp(const void* a, const void* b)
     return 0;
 }
 
+/* EDF: deadline ascending, then arrival, then id. */
+static int orc_cmp_edf(const void* a, const void* b)
+{
+    const orc_entry* x = (const orc_entry*)a;
+    const orc_entry* y = (const orc_entry*)b;
+    if (x->dl != y->dl) return x->dl < y->dl ? -1 : 1;
+    if (x->arrival != y->arrival) return x->arrival < y->arrival ? -1 : 1;
+    return x->id < y->id ? -1 : (x->id > y->id);
+}
+
+/* Naive aging: waiting time descending, then arrival, then id. */
+static int orc_cmp_age(const void* a, const void* b)
+{
+    const orc_entry* x = (const orc_entry*)a;
+    const orc_entry* y = (const orc_entry*)b;
+    if (x->dl != y->dl) return x->dl > y->dl ? -1 : 1;
+    if (x->arrival != y->arrival) return x->arrival < y->arrival ? -1 : 1;
+    return x->id < y->id ? -1 : (x->id > y->id);
+}
+
 int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
                  const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
                  const uint16_t* out, const uint8_t* mod, uint32_t* admit_seq,
@@ -169,7 +190,7 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
 {
     memset(cnt, 0, sizeof(*cnt));
     if (log_n) *log_n = 0;
-    if (r->chunk_budget == 0 || r->policy > ORC_TCM) return -1;
+    if (r->chunk_budget == 0 || r->policy > ORC_NAIVE_AGING || r->admit_skip > 1) return -1;
     for (uint32_t i = 0; i < n; ++i) {
         if (f[i] == 0 || f[i] > r->kv_capacity || out[i] == 0 || mod[i] > 2) return -1;
         if (i > 0 && arrival[i] < arrival[i - 1]) return -1;
@@ -227,14 +248,21 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
             uint32_t i = pending[q];
             order[q].id = i;
             order[q].arrival = arrival[i];
+            order[q].P = 0.0;
+            order[q].dl = 0;
             if (r->policy == ORC_TCM) {
                 int c = cls_out[i];
                 order[q].P = orc_priority(m->S[c], m->p[c], C[c], zero[c], clock - arrival[i]);
-            } else {
-                order[q].P = 0.0;
+            } else if (r->policy == ORC_EDF) {
+                order[q].dl = arrival[i] * m->slo_den +
+                              m->slo_num * orc_iso_e2e(m, r->chunk_budget, f[i], inl[i], out[i]);
+            } else if (r->policy == ORC_NAIVE_AGING) {
+                order[q].dl = clock - arrival[i];
             }
         }
         if (r->policy == ORC_TCM) qsort(order, n_pend, sizeof(orc_entry), orc_cmp);
+        if (r->policy == ORC_EDF) qsort(order, n_pend, sizeof(orc_entry), orc_cmp_edf);
+        if (r->policy == ORC_NAIVE_AGING) qsort(order, n_pend, sizeof(orc_entry), orc_cmp_age);
 
         /* 6 admission scan: greedy chunks; first KV misfit blocks later NEW admits (R6) */
         uint32_t left = Bp;
@@ -245,7 +273,7 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
             if (left == 0) break;
             if (!reserved[i]) {
                 if (blocked) continue;
-                if ((uint64_t)f[i] > kv_free) { blocked = 1; continue; }
+                if ((uint64_t)f[i] > kv_free) { blocked = !r->admit_skip; continue; }
                 reserved[i] = 1;
                 kv_free -= f[i];
                 admit_seq[i] = seq++;

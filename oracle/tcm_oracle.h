@@ -32,13 +32,20 @@ typedef struct {
     uint32_t slo_den;
 } orc_model;
 
-enum { ORC_FCFS = 0, ORC_TCM = 1 };
+/* FCFS: arrival order.  TCM: aging priority.
+ * EDF: earliest deadline first, deadline = arrival + (num/den) x isolated E2E (
+ * SPEC.md:399) -- ordering only, preemption is NEXT-1.  NAIVE_AGING: descending waiting time,
+ * ignoring class. */
+enum { ORC_FCFS = 0, ORC_TCM = 1, ORC_EDF = 2, ORC_NAIVE_AGING = 3 };
 
 typedef struct {
-    uint32_t policy;        /* ORC_FCFS or ORC_TCM                                 */
+    uint32_t policy;        /* ORC_*                                               */
     uint32_t chunk_budget;  /* B, chunked-prefill token budget      */
     uint64_t kv_capacity;   /* KV tokens               */
     double   alpha;         /* aging factor multiplying every k_c (R14)            */
+    uint32_t admit_skip;    /* 1: a KV misfit is skipped, later requests may still be
+                               admitted (first fit, NEXT-3); 0: it blocks them (R6) */
+    uint32_t pad;
 } orc_replica;
 
 typedef struct {

@@ -27,9 +27,14 @@ def classify(mod, f, thr):
     return 0 if f < mc else (1 if f < ct else 2)
 
 
+def iso_e2e(f, inl, out, B, c0=5000, cp=20, cd=500):
+    return inl + -(-f // B) * c0 + cp * f + (out - 1) * (c0 + cd)
+
+
 def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
-        thr=((4096, 2**32 - 1), (0, 2**32 - 1), (0, 8192))):
-    """reqs: list of (arrival_us, footprint, inline_us, out, modality). Returns dict of lists."""
+        thr=((4096, 2**32 - 1), (0, 2**32 - 1), (0, 8192)), skip=False, slo=5):
+    """reqs: list of (arrival_us, footprint, inline_us, out, modality); policy: 0 FCFS, 1 TCM,
+    2 EDF (deadline = arrival + slo x isolated E2E), 3 naive aging.  Returns dict of lists."""
     n = len(reqs)
     R = [dict(id=i, arr=a, f=f, inl=il, out=o, cls=classify(m, f, thr), state="future",
               rem=f, gen=0, admit=None, first=None, done=None)
@@ -56,6 +61,11 @@ def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
                 if ra["cls"] != rb["cls"] and abs(pa - pb) < 1e-11:
                     near_tie = True
             order = [r for _, r in sorted(keyed, key=lambda t: (-t[0], t[1]["arr"], t[1]["id"]))]
+        elif policy == 2:
+            dl = lambda r: r["arr"] + slo * iso_e2e(r["f"], r["inl"], r["out"], B, c0, cp, cd)
+            order = sorted(pend, key=lambda r: (dl(r), r["arr"], r["id"]))
+        elif policy == 3:
+            order = sorted(pend, key=lambda r: (-(clock - r["arr"]), r["arr"], r["id"]))
         else:
             order = sorted(pend, key=lambda r: (r["arr"], r["id"]))
         left, blocked, tok, inl = budget, False, 0, 0     # step 6 (R6, R7)
@@ -66,7 +76,7 @@ def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
                 if blocked:
                     continue
                 if r["f"] > free:
-                    blocked = True
+                    blocked = not skip
                     continue
                 r["state"] = "partial"
                 free -= r["f"]
