@@ -53,10 +53,18 @@ typedef int32_t tcm_status;
                                unreachable under R6; see tcm_stats_host.first_bad_*)     */
 #define TCM_E_VERSION (-7)  /* abi_version mismatch                                      */
 
-enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1 };
+enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1, TCM_POLICY_EDF = 2, TCM_POLICY_NAIVE_AGING = 3 };
 /* FCFS: vLLM's single arrival-ordered queue with chunked prefill.
  * TCM : three class queues + aging priority.  Static priority
- *        is TCM with aging_alpha = 0 (R14). */
+ *        is TCM with aging_alpha = 0 (R14).
+ * EDF : earliest deadline first, deadline = arrival + (slo_num/slo_den) x isolated E2E
+ *       (SPEC.md:399); ordering only, no preemption (NEXT-1).  STEPWISE only:
+ *       its keys are not class-monotone (Lemma L1 does not hold).
+ * NAIVE_AGING: descending waiting time ignoring class, i.e. arrival order. */
+
+/* tcm_replica_params.flags */
+#define TCM_ADMIT_SKIP 1u   /* a KV misfit is skipped instead of stopping new admissions (first
+                               fit; the alternative reading of R6, NEXT-3).  STEPWISE only. */
 
 enum { TCM_ENGINE_FUSED = 0, TCM_ENGINE_STEPWISE = 1 };
 /* FUSED   : one persistent thread per replica runs the whole step loop in registers;
@@ -93,7 +101,7 @@ typedef struct tcm_replica_params {
     uint64_t kv_capacity;  /* KV tokens, 1 .. 2^32-1    */
     double aging_alpha;    /* multiplies every k_c, >= 0 (R14)                      */
     uint32_t cell_id;      /* < n_cells: aggregation cell                           */
-    uint32_t reserved;     /* must be 0                                             */
+    uint32_t flags;        /* TCM_ADMIT_SKIP or 0                                    */
 } tcm_replica_params;
 
 /* The request trace, SoA in CSR form: replica r owns requests [req_offset[r], req_offset[r+1]),

@@ -113,7 +113,7 @@ size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) 
  b += (size_t)R * sizeof(ReplicaState);
     b += (size_t)R * sizeof(ClassPack);
     b += 20 * N;                                 // results kept on device when not supplied
-    if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N);
+    if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N) + 8 * N;
     if (host_mirror) b += (size_t)(R + 1) * 8 + 19 * N + (size_t)R * sizeof(tcm_replica_params);
     return b;
 }
@@ -294,6 +294,8 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         t.req_state = (uint8_t*)p;
         if ((st = dalloc(c, &p, stepwise_extra_bytes(R, N)))) return st;
         c->sw = stepwise_bind(p, R);
+        if ((st = dalloc(c, &p, 8 * (N ? N : 1)))) return st;
+        t.deadline = (uint64_t*)p;
     }
 
     c->t = t;
@@ -305,7 +307,7 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     // validate on the device (R18)
     uint32_t hv[2] = {0, 0xFFFFFFFFu};
     TCM_CUDA(c, cudaMemcpyAsync(c->d_val, hv, 8, cudaMemcpyHostToDevice, s));
-    launch_validate(t, c->d_val, s);
+    launch_validate(t, c->d_val, c->cfg.engine == TCM_ENGINE_STEPWISE, s);
     c->launches++;
     TCM_CUDA(c, cudaGetLastError());
     TCM_CUDA(c, cudaMemcpyAsync(hv, c->d_val, 8, cudaMemcpyDeviceToHost, s));
@@ -314,7 +316,8 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         return fail(c, TCM_E_CAPACITY, "replica %u: a footprint exceeds kv_capacity (R18)", hv[1]);
     if (hv[0] != ST_OK)
         return fail(c, TCM_E_ARG, "replica %u: malformed trace or params (footprint/out/modality/"
-                    "arrival order/policy/budget/kv/alpha)", hv[1]);
+                    "arrival order/policy/budget/kv/alpha/flags; EDF and TCM_ADMIT_SKIP need the "
+                    "stepwise engine)", hv[1]);
     launch_kpack(c->m, t, s);                 // params are validated: K1 class constants once
     c->launches++;
     TCM_CUDA(c, cudaGetLastError());

@@ -66,7 +66,7 @@ __global__ void k_kpack(ModelConst m, TraceDev t) {
 // ---------------------------------------------------------------------------------------
 // Validation: one warp per replica, lanes stride its requests (coalesced).
 // v[0] = worst status code (max), v[1] = first bad replica (min).
-__global__ void k_validate(TraceDev t, uint32_t* v) {
+__global__ void k_validate(TraceDev t, uint32_t* v, int general_ok) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     if (warp >= t.R) return;
@@ -75,9 +75,11 @@ __global__ void k_validate(TraceDev t, uint32_t* v) {
     const uint64_t a = t.offset[r], b = t.offset[r + 1];
     uint32_t bad = ST_OK;
     if (b < a || b > t.N || b - a >= 0xFFFFFFFFull) bad = ST_BAD_INPUT;
-    if (p.policy > TCM_POLICY_TCM || p.chunk_budget == 0 || p.kv_capacity == 0 ||
-        p.kv_capacity > 0xFFFFFFFFull || !(p.aging_alpha >= 0.0) || p.reserved != 0)
+    if (p.policy > TCM_POLICY_NAIVE_AGING || p.chunk_budget == 0 || p.kv_capacity == 0 ||
+        p.kv_capacity > 0xFFFFFFFFull || !(p.aging_alpha >= 0.0) || (p.flags & ~TCM_ADMIT_SKIP) != 0)
         bad = ST_BAD_INPUT;
+    // EDF and first-fit admission break Lemmas L1/L2: only the stepwise engine runs them
+    if (!general_ok && (p.policy == TCM_POLICY_EDF || (p.flags & TCM_ADMIT_SKIP))) bad = ST_BAD_INPUT;
     if (bad == ST_OK) {
         for (uint64_t i = a + lane; i < b; i += 32) {
             const uint32_t f = t.footprint[i];
@@ -323,9 +325,9 @@ void launch_kpack(const ModelConst& m, const TraceDev& t, cudaStream_t s) {
 void launch_init(const TraceDev& t, cudaStream_t s) {
     k_init<<<(t.R + 127) / 128, 128, 0, s>>>(t);
 }
-void launch_validate(const TraceDev& t, uint32_t* v, cudaStream_t s) {
+void launch_validate(const TraceDev& t, uint32_t* v, int general_ok, cudaStream_t s) {
     const uint64_t threads = (uint64_t)t.R * 32;
-    k_validate<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(t, v);
+    k_validate<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(t, v, general_ok);
 }
 void launch_reduce(const TraceDev& t, unsigned long long* acc, cudaStream_t s) {
     k_reduce<<<(t.R + 255) / 256, 256, 0, s>>>(t, acc);

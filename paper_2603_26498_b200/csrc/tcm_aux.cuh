@@ -12,7 +12,7 @@ enum : int {
 
 void launch_init(const TraceDev& t, cudaStream_t s);
 void launch_kpack(const ModelConst& m, const TraceDev& t, cudaStream_t s);
-void launch_validate(const TraceDev& t, uint32_t* v, cudaStream_t s);
+void launch_validate(const TraceDev& t, uint32_t* v, int general_ok, cudaStream_t s);
 void launch_reduce(const TraceDev& t, unsigned long long* acc, cudaStream_t s);
 void launch_aggregate(const ModelConst& m, const TraceDev& t, unsigned long long* hist,
                       unsigned long long* cnt, cudaStream_t s);

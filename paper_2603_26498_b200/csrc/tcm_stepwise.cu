@@ -186,6 +186,7 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
     const uint8_t* mod = t.mod + base;
     uint8_t* rs = t.req_state + base;
     const bool prio = t.params[r].policy == TCM_POLICY_TCM;
+    const bool edf = t.params[r].policy == TCM_POLICY_EDF;
     int mode = 0;
     if (!(st.flags & FLAG_FINISHED) && st.head[1] > 0) {
         const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};
@@ -205,6 +206,12 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
                     if (in[j]) {
                         const int c = prio ? classify(m, mod[i], fp[i]) : 0;
                         rs[i] = (uint8_t)(c | RS_PEND);
+                        if (edf) {   // EDF key input: deadline x den = arrival*den + num*iso_e2e
+                            const uint64_t f = fp[i], B = t.params[r].chunk_budget;
+                            const uint64_t iso = (uint64_t)t.inl[base + i] + (f + B - 1) / B * m.c0 + m.cp * f +
+                                                 (uint64_t)(t.out[base + i] - 1) * (m.c0 + m.cd);
+                            t.deadline[base + i] = arr[i] * m.slo_den + m.slo_num * iso;
+                        }
                     }
                     cnt += __popc(__ballot_sync(0xFFFFFFFFu, in[j]));
                 }
@@ -286,8 +293,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
 
         const tcm_replica_params prm = t.params[r];
         const bool prio = prm.policy == TCM_POLICY_TCM;
+        const bool edf = prm.policy == TCM_POLICY_EDF;
+        const bool skip = (prm.flags & TCM_ADMIT_SKIP) != 0;
         const uint64_t base = t.offset[r];
-        const uint64_t* arr = t.arrival + base;
+        // the streamed 8-byte key input: arrival (TCM aging, FCFS) or the EDF deadline x den
+        const uint64_t* arr = (edf ? t.deadline : t.arrival) + base;
         const uint32_t* fp = t.footprint + base;
         const uint32_t* inl = t.inl + base;
         const uint8_t* rsc = t.req_state + base;
@@ -461,13 +471,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                         }
                         qbits |= need ? (1u << j) : 0u;
                     } else if (!prio) {
-                        // FCFS: every key is 0, the order is the id order (R4)
-                        any_direct |= valid && !(has_th && (uint32_t)e <= thi) && (uint32_t)e < ki;
+                        // exact keys without K1: FCFS / naive aging (key 0, id order, R4) or EDF
+                        // (static key ~(deadline x den): earliest deadline first)
+                        const uint64_t key = edf ? ~a4[j] : 0;
+                        any_direct |= valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
+                                      before(key, (uint32_t)e, kk, ki);
                         if (valid && first_pass && (sb & RS_RES)) {
                             const int slot = atomicAdd(&sm.npart, 1);
                             if (slot < kMaxPart) {
                                 sm.part[slot] = (uint32_t)e;
-                                sm.partkey[slot] = 0;
+                                sm.partkey[slot] = key;
                             }
                         }
                     } else {
@@ -480,7 +493,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                         const int e = e0 + j;
                         const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
                         const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
-                        take(0, (uint32_t)e, valid && !(has_th && (uint32_t)e <= thi) && before(0, (uint32_t)e, kk, ki));
+                        const uint64_t key = edf ? ~a4[j] : 0;
+                        take(key, (uint32_t)e, valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
+                                                  before(key, (uint32_t)e, kk, ki));
                     }
                 }
                 if (__any_sync(0xFFFFFFFFu, qbits != 0)) {
@@ -555,15 +570,30 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     il = res ? 0 : inl[li];
                 }
                 const bool waiting = valid && !res;
-                const uint64_t cumf = warp_incl_scan64(waiting ? f : 0, lane);
-                const bool kv_ok = waiting && !blocked_prev && cumf <= kv;
+                bool kv_ok;
+                if (!skip) {
+                    // R6: admitted waiting requests form the prefix whose footprints fit
+                    const uint64_t cumf = warp_incl_scan64(waiting ? f : 0, lane);
+                    kv_ok = waiting && !blocked_prev && cumf <= kv;
+                } else {
+                    // first fit (NEXT-3): each waiting request in order takes KV if it still fits
+                    uint64_t kvl = kv;
+                    kv_ok = false;
+                    for (int l = 0; l < 32; ++l) {
+                        const uint32_t fl = __shfl_sync(0xFFFFFFFFu, f, l);
+                        const bool wl = __shfl_sync(0xFFFFFFFFu, waiting, l);
+                        const bool ok = wl && (uint64_t)fl <= kvl;
+                        kvl -= ok ? fl : 0;
+                        if (lane == l) kv_ok = ok;
+                    }
+                }
                 const bool part = valid && (res || kv_ok);
                 const uint64_t incl = warp_incl_scan64(part ? rr : 0, lane);
                 const uint64_t excl = incl - (part ? rr : 0);
                 const bool reached = excl < left;
                 const uint64_t chunk = (part && reached) ? (rr < left - excl ? rr : left - excl) : 0;
                 const bool admitted = kv_ok && reached;
-                const bool misfit = waiting && !blocked_prev && !kv_ok && reached;
+                const bool misfit = !skip && waiting && !blocked_prev && !kv_ok && reached;
                 const uint32_t adm_mask = __ballot_sync(0xFFFFFFFFu, admitted);
                 const uint32_t rank = __popc(adm_mask & ((1u << lane) - 1));
                 if (admitted) {

@@ -19,7 +19,8 @@ TCM_ABI_VERSION = 1
 TCM_OK = 0
 ERRORS = {-1: "TCM_E_ARG", -2: "TCM_E_STATE", -3: "TCM_E_CAPACITY", -4: "TCM_E_CUDA",
           -5: "TCM_E_OOM", -6: "TCM_E_REPLICA", -7: "TCM_E_VERSION"}
-POLICY_FCFS, POLICY_TCM = 0, 1
+POLICY_FCFS, POLICY_TCM, POLICY_EDF, POLICY_NAIVE_AGING = 0, 1, 2, 3
+ADMIT_SKIP = 1
 ENGINE_FUSED, ENGINE_STEPWISE = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 HIST_BINS, GROUPS, NCNT = 496, 4, 6
@@ -72,7 +73,7 @@ class tcm_stats_host(ctypes.Structure):
 
 # tcm_replica_params (32 B) as a numpy record so whole sweeps are built vectorised.
 PARAMS_DTYPE = np.dtype([("policy", "<u4"), ("chunk_budget", "<u4"), ("kv_capacity", "<u8"),
-                         ("aging_alpha", "<f8"), ("cell_id", "<u4"), ("reserved", "<u4")])
+                         ("aging_alpha", "<f8"), ("cell_id", "<u4"), ("flags", "<u4")])
 assert PARAMS_DTYPE.itemsize == 32
 
 _lib = None

@@ -255,3 +255,38 @@ def test_filter_bound_within_delta(alpha):
         e1 = tcm.tcm_k1_filter_error(tcm.config(), c, alpha, 0, 2**28, 1)
         e2 = tcm.tcm_k1_filter_error(tcm.config(), c, alpha, 0, 2**36, 97)
         assert max(e1, e2) < 1e-5, (c, alpha, e1, e2)
+
+
+# ------------------------------------------------------------------------------- NEXT-3
+def test_next3_policies_stepwise_bit_exact():
+    # EDF, naive aging and first-fit admission on the stepwise
+    # engine (general top-k path) vs the oracle
+    tr, params = sweep(160, 400, 61, kvs=(131072, 16384), rates=(1.0, 4.0))
+    rng = np.random.default_rng(3)
+    params["policy"] = rng.choice([tcm.POLICY_EDF, tcm.POLICY_NAIVE_AGING, tcm.POLICY_TCM, tcm.POLICY_FCFS], 160)
+    params["flags"] = rng.choice([0, tcm.ADMIT_SKIP], 160)
+    _, out, st = run_gpu(tr, params, tcm.ENGINE_STEPWISE)
+    assert st["requests_done"] == tr.n_requests
+    for r in range(160):
+        a, b = int(tr.offset[r]), int(tr.offset[r + 1])
+        o = O.simulate_trace(tr, r, policy=int(params["policy"][r]), alpha=float(params["aging_alpha"][r]),
+                             kv_capacity=int(params["kv_capacity"][r]), chunk_budget=int(params["chunk_budget"][r]),
+                             admit_skip=bool(params["flags"][r]))
+        assert o.status == 0
+        np.testing.assert_array_equal(out["admit_seq"][a:b], o.admit_seq, err_msg=f"replica {r}")
+        np.testing.assert_array_equal(out["first_token_us"][a:b], o.first_token_us, err_msg=f"replica {r}")
+        np.testing.assert_array_equal(out["done_us"][a:b], o.done_us, err_msg=f"replica {r}")
+
+
+def test_next3_naive_aging_fused_and_rejections():
+    tr, params = sweep(32, 300, 62)
+    params["policy"] = tcm.POLICY_NAIVE_AGING
+    _, out, _ = run_gpu(tr, params, tcm.ENGINE_FUSED)
+    check_replicas(tr, params, out, range(32))
+    # the fused engine relies on Lemmas L1/L2, which EDF and first-fit break: refused loudly
+    for pol, fl in ((tcm.POLICY_EDF, 0), (tcm.POLICY_TCM, tcm.ADMIT_SKIP)):
+        p2 = params.copy()
+        p2["policy"], p2["flags"] = pol, fl
+        with pytest.raises(tcm.TcmError) as e:
+            run_gpu(tr, p2, tcm.ENGINE_FUSED)
+        assert e.value.code == -1
