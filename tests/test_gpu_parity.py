@@ -290,3 +290,16 @@ def test_next3_naive_aging_fused_and_rejections():
         with pytest.raises(tcm.TcmError) as e:
             run_gpu(tr, p2, tcm.ENGINE_FUSED)
         assert e.value.code == -1
+
+
+def test_calibrated_thresholds_bit_exact():
+    # NEXT-4: thresholds learned by the calibration pipeline drive both engines (R13)
+    from paper_2603_26498_b200 import calibration as K
+    cal = T.generate(np.array([T.make_replica(42, r, 300, 1.0, (1 / 3, 1 / 3, 1 / 3), 131072) for r in range(3)]))
+    thr, _, _ = K.calibrate(cal)
+    tr, params = sweep(64, 300, 63)
+    m = O.model(thresholds=thr)
+    for engine in ENGINES:
+        cfg = tcm.config(engine=engine, thresholds=thr)
+        _, out, _ = run_gpu(tr, params, engine, cfg=cfg)
+        check_replicas(tr, params, out, range(64), m=m)
