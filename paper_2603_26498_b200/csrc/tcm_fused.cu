@@ -246,104 +246,6 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
             ex[c] = !prio;
             pf[c] = (prio && cur[c] != NIL) ? bound(c, st.clock - carr[c]) : 0.0f;
         }
-        // ---- Lemma L4c: the top-ranked head misfits and nothing is partial, and every head that
-        // would fit ranks below the top's priority *now* even at the start of the last iteration
-        // before the next finish / arrival.  Priorities only grow with waiting time (L1), so the top
-        // stays on top through the window and every iteration in it is blocked (R6): take the
-        // window in closed form, exactly like L4.
-        if (prio && left > 0 && st.n_dec > 0 && (st.flags & 7u) == 0) {
-            const uint64_t dt = m.c0 + m.cd * st.n_dec;
-            uint64_t j = next_fin - st.iter;
-            if (next_arr != ~0ull) {
-                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
-                j = ja < j ? ja : j;
-            }
-            j = j < budget ? j : budget;
-            if (j >= 2) {
-                int top = -1;                                     // top-ranked head, exact order
-                uint64_t bk = 0, ba = 0;
-                uint32_t bi = 0;
-                float bpf = 0.0f;
-                bool bex = true;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    if (cur[c] != NIL) {
-                        bool better = top < 0;
-                        if (!better) {
-                            const float d = pf[c] - bpf;
-                            if (use_bound && d > 2.5e-4f) {
-                                better = true;
-                            } else if (use_bound && d < -2.5e-4f) {
-                                better = false;
-                            } else {
-                                if (!ex[c]) {
-                                    key[c] = k1_key(kc[c], st.clock - carr[c]);
-                                    ex[c] = true;
-                                }
-                                if (!bex) {
-#pragma unroll
-                                    for (int q = 0; q < c; ++q) {
-                                        if (q == top) {
-                                            key[q] = k1_key(kc[q], st.clock - carr[q]);
-                                            ex[q] = true;
-                                            bk = key[q];
-                                        }
-                                    }
-                                    bex = true;
-                                }
-                                better = key[c] > bk || (key[c] == bk && (carr[c] < ba || (carr[c] == ba && cur[c] < bi)));
-                            }
-                        }
-                        if (better) {
-                            top = c;
-                            bk = key[c];
-                            bex = ex[c];
-                            bpf = pf[c];
-                            ba = carr[c];
-                            bi = cur[c];
-                        }
-                    }
-                }
-                bool hold = false;
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    if (c == top) hold = (uint64_t)cf[c] > st.kv_free;
-                const uint64_t t_end = st.clock + (j - 1) * dt;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    if (hold && c != top && cur[c] != NIL && (uint64_t)cf[c] <= st.kv_free) {
-                        const float pe = bound(c, t_end - carr[c]);
-                        if (!(use_bound && bpf - pe > 2.5e-4f)) {
-                            if (!bex) {
-#pragma unroll
-                                for (int q = 0; q < 3; ++q) {
-                                    if (q == top) {
-                                        key[q] = k1_key(kc[q], st.clock - carr[q]);
-                                        ex[q] = true;
-                                        bk = key[q];
-                                    }
-                                }
-                                bex = true;
-                            }
-                            hold = bk > k1_key(kc[c], t_end - carr[c]);
-                        }
-                    }
-                }
-                if (hold) {
-                    st.clock += j * dt;
-                    st.iter += j;
-                    st.decisions += j;
-                    st.sum_pending += j * st.n_pend;
-                    st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
-                    budget -= (uint32_t)j;
-                    if (st.iter == next_fin) {
-                        cal_process(cal, link, st.iter, st.clock, fp, done, st);
-                        next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
-                    }
-                    continue;
-                }
-            }
-        }
         while (left > 0) {
             int best = -1;
             uint64_t bk = 0, ba = 0;
