@@ -113,7 +113,7 @@ size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) 
  b += (size_t)R * sizeof(ReplicaState);
     b += (size_t)R * sizeof(ClassPack);
     b += 20 * N;                                 // results kept on device when not supplied
-    if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N) + 8 * N + (size_t)R * 128;
+    if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N) + 8 * N;
     if (host_mirror) b += (size_t)(R + 1) * 8 + 19 * N + (size_t)R * sizeof(tcm_replica_params);
     return b;
 }
@@ -153,7 +153,6 @@ tcm_status reset_state(tcm_ctx* c) {
     TCM_CUDA(c, cudaMemsetAsync(t.done, 0, 8 * N, s));
     TCM_CUDA(c, cudaMemsetAsync(t.admit_seq, 0xFF, 4 * N, s));
     if (t.req_state) TCM_CUDA(c, cudaMemsetAsync(t.req_state, 0, N ? N : 1, s));
-    if (t.seeds) TCM_CUDA(c, cudaMemsetAsync(t.seeds, 0xFF, (size_t)R * 32 * 4, s));
     launch_init(t, s);
     c->launches++;
     if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
@@ -297,8 +296,6 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         c->sw = stepwise_bind(p, R);
         if ((st = dalloc(c, &p, 8 * (N ? N : 1)))) return st;
         t.deadline = (uint64_t*)p;
-        if ((st = dalloc(c, &p, (size_t)R * 32 * 4))) return st;
-        t.seeds = (uint32_t*)p;
     }
 
     c->t = t;

@@ -86,7 +86,6 @@ struct TraceDev {
     uint8_t* req_state;      // [N] stepwise engine: per-request class / phase byte
     ClassPack* kpack;        // [R] per-replica K1 class constants
     uint64_t* deadline;      // [N] stepwise engine, EDF: arrival*den + num*iso_e2e (set at ingest)
-    uint32_t* seeds;         // [R * 32] stepwise engine: previous iteration's top-32 ids
 };
 
 __device__ __forceinline__ int classify(const ModelConst& m, uint32_t mod, uint32_t f) {

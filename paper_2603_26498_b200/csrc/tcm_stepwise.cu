@@ -32,7 +32,7 @@ constexpr int kMaxPart = 32;
 constexpr uint32_t ST_PARTIAL_OVERFLOW = 4;
 
 // request-state byte
-constexpr uint8_t RS_CLS = 3, RS_PEND = 4, RS_RES = 8, RS_FT = 16, RS_SEED = 32;
+constexpr uint8_t RS_CLS = 3, RS_PEND = 4, RS_RES = 8, RS_FT = 16;
 
 // stream staging: per warp, kStages chunks of 128 requests (1 KB arrivals + 128 B states)
 constexpr int kStages = 3;
@@ -439,36 +439,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 }
                 cp_async_commit();
             };
-            // seed the list with the previous iteration's top-32 (exact keys at this clock) and
-            // mark them so the stream skips them; any request may be seeded -- the selected set is
-            // still the top-32 of ALL pending requests, the seeds only tighten the threshold early
-            uint32_t seed_id = NIL;
-            bool seeded = false;
-            if (first_pass) {
-                if (wg == 0) {
-                    seed_id = t.seeds[(size_t)r * 32 + lane];
-                    const bool inwin = seed_id != NIL && seed_id >= lo && seed_id < hi;
-                    const uint32_t sb = inwin ? rsc[seed_id] : 0;
-                    seeded = inwin && (sb & RS_PEND);
-                    uint64_t key = 0;
-                    if (seeded) {
-                        const int c = sb & RS_CLS;
-                        if (prio) key = k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, clock - arr[seed_id], tb);
-                        else if (edf) key = ~arr[seed_id];
-                        if (sb & RS_RES) {
-                            const int slot = atomicAdd(&sm.npart, 1);
-                            if (slot < kMaxPart) {
-                                sm.part[slot] = seed_id;
-                                sm.partkey[slot] = key;
-                            }
-                        }
-                        rs[seed_id] = (uint8_t)(sb | RS_SEED);
-                    }
-                    take(key, seed_id, seeded);
-                    __syncwarp();
-                }
-                group_sync<G>();
-            }
             int64_t g0 = gstart + (int64_t)wg * 128;
 #pragma unroll
             for (int q = 0; q < kStages - 1; ++q) issue(g0 + q * stride, q);
@@ -487,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 for (int j = 0; j < 4; ++j) {
                     const int e = e0 + j;
                     const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                    const bool valid = (sb & RS_PEND) && !(sb & RS_SEED) && e >= (int)lo && e < (int)hi;
+                    const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
                     const int c = sb & RS_CLS;
                     if (lean) {
                         // skip when the exact cap or the FP32 bound proves rank after (kk, ki)
@@ -522,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     for (int j = 0; j < 4; ++j) {
                         const int e = e0 + j;
                         const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                        const bool valid = (sb & RS_PEND) && !(sb & RS_SEED) && e >= (int)lo && e < (int)hi;
+                        const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
                         const uint64_t key = edf ? ~a4[j] : 0;
                         take(key, (uint32_t)e, valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
                                                   before(key, (uint32_t)e, kk, ki));
@@ -585,11 +555,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 if (G > 1) {
 #pragma unroll 1
                     for (int w = 1; w < G; ++w) warp_merge(lk, li, sm.wkey[w][lane], sm.wid[w][lane], lane);
-                }
-                if (first_pass) {
-                    if (seeded) rs[seed_id] = (uint8_t)(rs[seed_id] & ~RS_SEED);   // before any re-stream
-                    t.seeds[(size_t)r * 32 + lane] = li;                            // next iteration's seeds
-                    __syncwarp();
                 }
                 const bool valid = li != NIL;
                 const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
