@@ -220,13 +220,15 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
             continue;
         }
 
-        // ---- a2 + a3 + a4: merge the class-FIFO heads by key, scan under token/KV budgets
+        // ---- a2 + a3 + a4: merge the class-FIFO heads by key, scan under token/KV budgets.
+        // The scan advances the queue heads in place; oh[c] keeps each old head for the
+        // first-token walk of a5.
         uint64_t tok = 0, inl_sum = 0;
         bool blocked = false;                               // R6
-        uint32_t cur[3], crem[3], cf[3], csid[3], csf[3];
-        uint64_t carr[3], key[3], csarr[3];
+        uint32_t oh[3];
+        uint64_t key[3];
         float pf[3];          // FP32 bound of each head's priority (|P~ - P| <= 1e-5)
-        bool cres[3], ex[3];  // ex[c]: key[c] holds the exact K1 key
+        bool ex[3];           // ex[c]: key[c] holds the exact K1 key
         // Two heads whose bounds are more than 2.5e-4 apart are ordered by the bounds (the exact
         // order, since the bound error is < 1e-5); only closer pairs get their exact FP64 keys.
         auto bound = [&](int c, uint64_t w) -> float {
@@ -234,17 +236,10 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
         };
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            cur[c] = st.head[c];
-            crem[c] = st.rem[c];
-            carr[c] = harr[c];
-            cf[c] = hf[c];
-            csid[c] = sid[c];
-            csarr[c] = sarr[c];
-            csf[c] = sf[c];
-            cres[c] = (st.flags >> c) & 1u;
+            oh[c] = st.head[c];
             key[c] = 0;
             ex[c] = !prio;
-            pf[c] = (prio && cur[c] != NIL) ? bound(c, st.clock - carr[c]) : 0.0f;
+            pf[c] = (prio && st.head[c] != NIL) ? bound(c, st.clock - harr[c]) : 0.0f;
         }
         while (left > 0) {
             int best = -1;
@@ -254,7 +249,7 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
             bool bex = true;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                if (cur[c] != NIL && (!blocked || cres[c])) {
+                if (st.head[c] != NIL && (!blocked || ((st.flags >> c) & 1u))) {
                     bool better = best < 0;
                     if (!better) {
                         const float d = pf[c] - bpf;
@@ -264,21 +259,22 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
                             better = false;
                         } else {
                             if (!ex[c]) {
-                                key[c] = k1_key(kc[c], st.clock - carr[c]);
+                                key[c] = k1_key(kc[c], st.clock - harr[c]);
                                 ex[c] = true;
                             }
                             if (!bex) {
 #pragma unroll
                                 for (int q = 0; q < c; ++q) {
                                     if (q == best) {
-                                        key[q] = k1_key(kc[q], st.clock - carr[q]);
+                                        key[q] = k1_key(kc[q], st.clock - harr[q]);
                                         ex[q] = true;
                                         bk = key[q];
                                     }
                                 }
                                 bex = true;
                             }
-                            better = key[c] > bk || (key[c] == bk && (carr[c] < ba || (carr[c] == ba && cur[c] < bi)));
+                            better = key[c] > bk ||
+                                     (key[c] == bk && (harr[c] < ba || (harr[c] == ba && st.head[c] < bi)));
                         }
                     }
                     if (better) {
@@ -286,8 +282,8 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
                         bk = key[c];
                         bex = ex[c];
                         bpf = pf[c];
-                        ba = carr[c];
-                        bi = cur[c];
+                        ba = harr[c];
+                        bi = st.head[c];
                     }
                 }
             }
@@ -295,40 +291,40 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (c == best) {
-                    const uint32_t i = cur[c];
+                    const uint32_t i = st.head[c];
                     bool go = true;
-                    if (!cres[c]) {
-                        if ((uint64_t)cf[c] > st.kv_free) {
+                    if (!((st.flags >> c) & 1u)) {
+                        if ((uint64_t)hf[c] > st.kv_free) {
                             blocked = true;                 // first misfit stops new admits
                             go = false;
                         } else {
-                            st.kv_free -= cf[c];            // R7 reserve the full footprint
+                            st.kv_free -= hf[c];            // R7 reserve the full footprint
                             admit[i] = st.seq++;
                             inl_sum += inl[i];              // R10
-                            cres[c] = true;
+                            st.flags |= 1u << c;
                         }
                     }
                     if (go) {
-                        const uint32_t ch = crem[c] < left ? crem[c] : left;
-                        crem[c] -= ch;
+                        const uint32_t ch = st.rem[c] < left ? st.rem[c] : left;
+                        st.rem[c] -= ch;
                         left -= ch;
                         tok += ch;
-                        if (crem[c] == 0) {                 // prefill complete: next in FIFO
+                        if (st.rem[c] == 0) {               // prefill complete: next in FIFO
+                            st.flags &= ~(1u << c);
                             if (i == st.tail[c]) {
-                                cur[c] = NIL;
-                                csid[c] = NIL;
+                                st.head[c] = NIL;
+                                sid[c] = NIL;
                             } else {
-                                const uint32_t ni = csid[c];   // prefetched successor
-                                cur[c] = ni;
-                                carr[c] = csarr[c];
-                                cf[c] = csf[c];
-                                crem[c] = cf[c];
-                                cres[c] = false;
+                                const uint32_t ni = sid[c];    // prefetched successor
+                                st.head[c] = ni;
+                                harr[c] = sarr[c];
+                                hf[c] = sf[c];
+                                st.rem[c] = hf[c];
                                 ex[c] = !prio;
-                                if (prio) pf[c] = bound(c, st.clock - carr[c]);
-                                csid[c] = ni != st.tail[c] ? link[ni] : NIL;
-                                csarr[c] = csid[c] != NIL ? arr[csid[c]] : 0;
-                                csf[c] = csid[c] != NIL ? fp[csid[c]] : 0;
+                                if (prio) pf[c] = bound(c, st.clock - harr[c]);
+                                sid[c] = ni != st.tail[c] ? link[ni] : NIL;
+                                sarr[c] = sid[c] != NIL ? arr[sid[c]] : 0;
+                                sf[c] = sid[c] != NIL ? fp[sid[c]] : 0;
                             }
                         }
                     }
@@ -356,8 +352,8 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            uint32_t i = st.head[c];
-            while (i != cur[c]) {
+            uint32_t i = oh[c];
+            while (i != st.head[c]) {
                 const uint32_t ni = (i == st.tail[c]) ? NIL : link[i];
                 first[i] = st.clock;
                 st.n_pend--;
@@ -374,15 +370,7 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
                 }
                 i = ni;
             }
-            st.head[c] = cur[c];
-            if (cur[c] == NIL) st.tail[c] = NIL;
-            st.rem[c] = crem[c];
-            st.flags = cres[c] ? (st.flags | (1u << c)) : (st.flags & ~(1u << c));
-            harr[c] = carr[c];
-            hf[c] = cf[c];
-            sid[c] = csid[c];
-            sarr[c] = csarr[c];
-            sf[c] = csf[c];
+            if (st.head[c] == NIL) st.tail[c] = NIL;
         }
         if (recompute_fin) next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
     }
