@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
     uint64_t next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
     uint64_t next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
     uint32_t budget = max_iters;
+    bool arm = false;     // the previous decision was blocked: try Lemma L4c once
 
     for (;;) {
         // ---- a1: ingest arrivals <= clock; classify; append to the class FIFO
@@ -197,6 +198,40 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
 #pragma unroll
             for (int c = 0; c < 3; ++c)
                 if (st.head[c] != NIL && (((st.flags >> c) & 1u) || (uint64_t)hf[c] <= st.kv_free)) stuck = false;
+        }
+        // L4c: some head that does not fit ranks, *now*, above every head that fits even at the
+        // start of the window's last iteration.  Priorities only grow with waiting time (L1), so
+        // at every iteration of the window the top-ranked head misfits and blocks all admissions
+        // (R6); with no partial (flags) nothing prefills.  FP32 bounds only (rigorous, 2.5e-4
+        // margin); tried once after a blocked decision.
+        if (!stuck && arm && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
+            arm = false;
+            const uint64_t dt = m.c0 + m.cd * st.n_dec;
+            uint64_t j = next_fin - st.iter;
+            if (next_arr != ~0ull) {
+                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+                j = ja < j ? ja : j;
+            }
+            j = j < budget ? j : budget;
+            if (j >= 2) {
+                const uint64_t t_end = st.clock + (j - 1) * dt;
+                float ptop = -1.0f, pfit = -1.0f;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (st.head[c] == NIL || kc[c].zero) continue;
+                    if ((uint64_t)hf[c] > st.kv_free) {
+                        const float p = k1_filter_f32(fS[c], fp2[c], fC2[c], st.clock - harr[c]);
+                        ptop = p > ptop ? p : ptop;
+                    } else {
+                        const float p = k1_filter_f32(fS[c], fp2[c], fC2[c], t_end - harr[c]);
+                        pfit = p > pfit ? p : pfit;
+                    }
+                }
+                bool zero_head = false;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) zero_head |= st.head[c] != NIL && kc[c].zero;
+                stuck = !zero_head && ptop >= 0.0f && ptop - pfit > 2.5e-4f;
+            }
         }
         if (stuck && st.n_dec > 0) {
             const uint64_t F = next_fin;
@@ -331,6 +366,7 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
                 }
             }
         }
+        arm = tok == 0 && blocked;
         if (tok == 0 && st.n_dec == 0) {                    // unreachable under R6
             st.status = ST_DEADLOCK;
             st.flags |= FLAG_FINISHED;
