@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
         // at every iteration of the window the top-ranked head misfits and blocks all admissions
         // (R6); with no partial (flags) nothing prefills.  FP32 bounds only (rigorous, 2.5e-4
         // margin); tried once after a blocked decision.
+        uint64_t l4c_j = ~0ull;
         if (!stuck && arm && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
             arm = false;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
@@ -213,24 +214,33 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
                 j = ja < j ? ja : j;
             }
             j = j < budget ? j : budget;
-            if (j >= 2) {
+            bool zero_head = false;
+            float ptop = -1.0f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                zero_head |= st.head[c] != NIL && kc[c].zero;
+                if (st.head[c] != NIL && !kc[c].zero && (uint64_t)hf[c] > st.kv_free) {
+                    const float p = k1_filter_f32(fS[c], fp2[c], fC2[c], st.clock - harr[c]);
+                    ptop = p > ptop ? p : ptop;
+                }
+            }
+            // the longest window (halving from the full one) over which every fitting head stays
+            // below the best misfitting head's priority now
+            for (int h = 0; h < 6 && j >= 2 && !zero_head && ptop >= 0.0f; ++h, j >>= 1) {
                 const uint64_t t_end = st.clock + (j - 1) * dt;
-                float ptop = -1.0f, pfit = -1.0f;
+                float pfit = -1.0f;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    if (st.head[c] == NIL || kc[c].zero) continue;
-                    if ((uint64_t)hf[c] > st.kv_free) {
-                        const float p = k1_filter_f32(fS[c], fp2[c], fC2[c], st.clock - harr[c]);
-                        ptop = p > ptop ? p : ptop;
-                    } else {
+                    if (st.head[c] != NIL && (uint64_t)hf[c] <= st.kv_free) {
                         const float p = k1_filter_f32(fS[c], fp2[c], fC2[c], t_end - harr[c]);
                         pfit = p > pfit ? p : pfit;
                     }
                 }
-                bool zero_head = false;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) zero_head |= st.head[c] != NIL && kc[c].zero;
-                stuck = !zero_head && ptop >= 0.0f && ptop - pfit > 2.5e-4f;
+                if (ptop - pfit > 2.5e-4f) {
+                    stuck = true;
+                    l4c_j = j;
+                    break;
+                }
             }
         }
         if (stuck && st.n_dec > 0) {
@@ -242,6 +252,7 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
                 j = ja < j ? ja : j;
             }
             j = j < budget ? j : budget;
+            j = j < l4c_j ? j : l4c_j;
             st.clock += j * dt;
             st.iter += j;
             st.decisions += j;
@@ -252,6 +263,7 @@ __global__ void __launch_bounds__(64, 8) k_fused(ModelConst m, TraceDev t, uint3
                 cal_process(cal, link, st.iter, st.clock, fp, done, st);
                 next_fin = st.n_dec > 0 ? cal_next(cal, st.iter) : ~0ull;
             }
+            arm = true;                                     // still blocked: try L4c again next
             continue;
         }
 
