@@ -69,6 +69,7 @@ enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1, TCM_POLICY_EDF = 2, TCM_POLICY_N
 enum { TCM_ENGINE_FUSED = 0, TCM_ENGINE_STEPWISE = 1 };
 /* FUSED   : one persistent thread per replica runs the whole step loop in registers;
  *           a3 is the exact 3-way merge of the class-FIFO heads (Lemma L1).
+ *           Replicas must hold < 2^24 requests (calendar slot counters).
  * STEPWISE: the paper-literal step -- per iteration, every pending request of every
  *           active replica is re-keyed (a1+a2), top-k selected (a3), prefix-scanned (a4),
  *           then the clock kernel runs (a5).  Bit-identical results; used for the
@@ -167,20 +168,25 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out);
 /* Binds a trace and result buffers, allocates the workspace (tcm_workspace_bytes) and
  * validates the trace on the device: footprint <= kv_capacity (TCM_E_CAPACITY), and
  * footprint >= 1, 1 <= out <= 2048, modality <= 2, non-decreasing arrivals, params in
- * range (TCM_E_ARG).  HOST traces are copied to the device here (on the stream).
+ * range, EDF / TCM_ADMIT_SKIP / >= 2^24 requests per replica only on the STEPWISE engine
+ * (TCM_E_ARG).  HOST traces are copied to the device here (on the stream).
  * Resets every replica to its initial state (clock 0, all KV free). */
 tcm_status tcm_load_trace(tcm_ctx* ctx, const tcm_trace_view* trace,
                           const tcm_results_view* results);
 
 /* Resets every replica of the bound trace to its initial state (clock 0, all KV free, no
  * request admitted) without re-validating or re-copying the trace: device work only
- * (memsets + one kernel), enqueued on the stream.  TCM_E_STATE before tcm_load_trace. */
+ * (memsets + two kernels: state init and the engine's prologue -- the FUSED engine
+ * classifies every request into its class segment here, row a1), enqueued on the stream.
+ * TCM_E_STATE before tcm_load_trace. */
 tcm_status tcm_reset(tcm_ctx* ctx);
 
 /* Advances every unfinished replica by at most max_iterations engine iterations (a
  * fast-forward counts all the iterations it covers; idle jumps count none).  Writes the
  * number of replicas still unfinished to *active_replicas (may be NULL).  HOST results
- * are copied back before returning. */
+ * are copied back before returning.  Afterwards every result of a request that has reached
+ * that stage is final; admit_seq / first_token_us / done_us of a request that has not are
+ * 0xFFFFFFFF / 0 / 0. */
 tcm_status tcm_step(tcm_ctx* ctx, uint32_t max_iterations, uint32_t* active_replicas);
 
 /* Runs every replica to completion (every request done).  TCM_E_REPLICA if a replica

@@ -107,10 +107,15 @@ ModelConst to_model(const tcm_config& c) {
 
 size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) {
     size_t b = 0;
-    b += 4 * N;                                  // link
-    b += (size_t)R * kCalSlots * 4;              // calendar heads
+    if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) {
+        b += 4 * N;                              // link
+        b += (size_t)R * kCalSlots * 4;          // calendar slot list heads
+    } else {
+        b += (sizeof(FRec) + 16 + 8) * N;        // class-segment records, finish-event log, finish iterations
+        b += (size_t)R * kCalSlots * 8;          // calendar slot counters
+    }
     b += (size_t)R * kCalWords * 4;              // occupancy
- b += (size_t)R * sizeof(ReplicaState);
+    b += (size_t)R * sizeof(ReplicaState);
     b += (size_t)R * sizeof(ClassPack);
     b += 20 * N;                                 // results kept on device when not supplied
     if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N) + 8 * N;
@@ -147,7 +152,9 @@ tcm_status reset_state(tcm_ctx* c) {
     cudaStream_t s = c->s;
     const uint32_t R = t.R;
     const uint64_t N = t.N;
-    TCM_CUDA(c, cudaMemsetAsync(t.cal, 0xFF, (size_t)R * kCalSlots * 4, s));
+    if (t.cal) TCM_CUDA(c, cudaMemsetAsync(t.cal, 0xFF, (size_t)R * kCalSlots * 4, s));
+    if (t.fw.cal) TCM_CUDA(c, cudaMemsetAsync(t.fw.cal, 0, (size_t)R * kCalSlots * 8, s));
+    if (t.fw.fin) TCM_CUDA(c, cudaMemsetAsync(t.fw.fin, 0, 8 * (N ? N : 1), s));
     TCM_CUDA(c, cudaMemsetAsync(t.occ, 0, (size_t)R * kCalWords * 4, s));
     TCM_CUDA(c, cudaMemsetAsync(t.first_token, 0, 8 * N, s));
     TCM_CUDA(c, cudaMemsetAsync(t.done, 0, 8 * N, s));
@@ -158,6 +165,9 @@ tcm_status reset_state(tcm_ctx* c) {
     if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
         stepwise_init(t, s);
         c->launches++;
+    } else {
+        launch_fused_prologue(c->m, t, s);      // a1: class segments
+        c->launches++;
     }
     TCM_CUDA(c, cudaGetLastError());
     return TCM_OK;
@@ -167,7 +177,8 @@ tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
     TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
     if (c->cfg.engine == TCM_ENGINE_FUSED) {
         launch_fused(c->m, c->t, max_iters, c->d_active, c->s);
-        c->launches++;
+        launch_fused_stamp(c->t, c->s);
+        c->launches += 2;
     } else {
         uint64_t l = 0;
         tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, &l);
@@ -279,10 +290,21 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     else { if ((st = dalloc(c, &p, 8 * N))) return st; t.done = (uint64_t*)p; }
 
     // workspace
-    if ((st = dalloc(c, &p, 4 * N))) return st;
-    t.link = (uint32_t*)p;
-    if ((st = dalloc(c, &p, (size_t)R * kCalSlots * 4))) return st;
-    t.cal = (uint32_t*)p;
+    if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
+        if ((st = dalloc(c, &p, 4 * N))) return st;
+        t.link = (uint32_t*)p;
+        if ((st = dalloc(c, &p, (size_t)R * kCalSlots * 4))) return st;
+        t.cal = (uint32_t*)p;
+    } else {
+        if ((st = dalloc(c, &p, sizeof(FRec) * N))) return st;
+        t.fw.rec = (FRec*)p;
+        if ((st = dalloc(c, &p, 16 * N))) return st;
+        t.fw.log = (uint64_t*)p;
+        if ((st = dalloc(c, &p, 8 * N))) return st;
+        t.fw.fin = (uint64_t*)p;
+        if ((st = dalloc(c, &p, (size_t)R * kCalSlots * 8))) return st;
+        t.fw.cal = (uint64_t*)p;
+    }
     if ((st = dalloc(c, &p, (size_t)R * kCalWords * 4))) return st;
     t.occ = (uint32_t*)p;
     if ((st = dalloc(c, &p, (size_t)R * sizeof(ReplicaState)))) return st;
@@ -299,12 +321,8 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     }
 
     c->t = t;
-    {
-        tcm_status rs = reset_state(c);
-        if (rs != TCM_OK) return rs;
-    }
 
-    // validate on the device (R18)
+    // validate on the device (R18) before any kernel reads the trace
     uint32_t hv[2] = {0, 0xFFFFFFFFu};
     TCM_CUDA(c, cudaMemcpyAsync(c->d_val, hv, 8, cudaMemcpyHostToDevice, s));
     launch_validate(t, c->d_val, c->cfg.engine == TCM_ENGINE_STEPWISE, s);
@@ -316,11 +334,16 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         return fail(c, TCM_E_CAPACITY, "replica %u: a footprint exceeds kv_capacity (R18)", hv[1]);
     if (hv[0] != ST_OK)
         return fail(c, TCM_E_ARG, "replica %u: malformed trace or params (footprint/out/modality/"
-                    "arrival order/policy/budget/kv/alpha/flags; EDF and TCM_ADMIT_SKIP need the "
+                    "arrival order/policy/budget/kv/alpha/flags; EDF, TCM_ADMIT_SKIP and replicas of "
+                    ">= 2^24 requests need the "
                     "stepwise engine)", hv[1]);
     launch_kpack(c->m, t, s);                 // params are validated: K1 class constants once
     c->launches++;
     TCM_CUDA(c, cudaGetLastError());
+    {
+        tcm_status rs = reset_state(c);
+        if (rs != TCM_OK) return rs;
+    }
     c->loaded = true;
     c->err.clear();
     return TCM_OK;

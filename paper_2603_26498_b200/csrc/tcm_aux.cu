@@ -80,6 +80,8 @@ __global__ void k_validate(TraceDev t, uint32_t* v, int general_ok) {
         bad = ST_BAD_INPUT;
     // EDF and first-fit admission break Lemmas L1/L2: only the stepwise engine runs them
     if (!general_ok && (p.policy == TCM_POLICY_EDF || (p.flags & TCM_ADMIT_SKIP))) bad = ST_BAD_INPUT;
+    // fused calendar slots count finishing requests in 24 bits
+    if (!general_ok && b - a >= (1ull << (64 - kCalCntShift))) bad = ST_BAD_INPUT;
     if (bad == ST_OK) {
         for (uint64_t i = a + lane; i < b; i += 32) {
             const uint32_t f = t.footprint[i];

@@ -36,7 +36,8 @@ struct __align__(16) ReplicaState {
     uint64_t decisions;      // R17
     uint64_t sum_pending;
     uint64_t ff_iters;
-    uint64_t idle_jumps;
+    uint32_t idle_jumps;
+    uint32_t nlog;           // fused engine: finish-event log entries (FusedWs::log)
     uint32_t done_count;
     uint32_t scanned;        // decisions that ran the full key/merge/scan (not fast-forwarded)
 };
@@ -64,6 +65,29 @@ struct ModelConst {
     uint32_t n_cells;
 };
 
+// Fused engine: one request as it sits in its class segment.  The prologue
+// (k_fpack, rows a1) classifies every request once and lays replica r's requests out as three
+// contiguous class segments, each in arrival order (Lemma L1: the class FIFO), so a queue head's
+// successor is the next record and one 256-bit load fetches everything the loop needs.
+struct __align__(32) FRec {
+    uint64_t arrival;        // arrival_us
+    uint32_t fp;             // footprint
+    uint32_t inl;            // inline_us
+    uint32_t id;             // local request id (index into the trace / results)
+    uint32_t out;            // out_tokens
+    uint64_t spare;
+};
+static_assert(sizeof(FRec) == 32, "FRec is one 32-byte sector");
+
+// Fused engine workspace.
+struct FusedWs {
+    FRec* rec;               // [N] class segments per replica
+    uint64_t* cal;           // [R * kCalSlots] per iteration slot: (finishing count << 40) | sum of footprints
+    uint64_t* log;           // [2N] per replica (iteration, clock) of every finish event, in order
+    uint64_t* fin;           // [N] finish iteration of a decoding request (0: none pending)
+};
+constexpr int kCalCntShift = 40;
+
 // Everything a kernel needs about the bound trace (device pointers).
 struct TraceDev {
     uint32_t R;
@@ -86,6 +110,7 @@ struct TraceDev {
     uint8_t* req_state;      // [N] stepwise engine: per-request class / phase byte
     ClassPack* kpack;        // [R] per-replica K1 class constants
     uint64_t* deadline;      // [N] stepwise engine, EDF: arrival*den + num*iso_e2e (set at ingest)
+    FusedWs fw;              // fused engine only
 };
 
 __device__ __forceinline__ int classify(const ModelConst& m, uint32_t mod, uint32_t f) {
@@ -93,7 +118,9 @@ __device__ __forceinline__ int classify(const ModelConst& m, uint32_t mod, uint3
     return f < m.thr_mc[mod] ? 0 : (f < m.thr_ct[mod] ? 1 : 2);
 }
 
+void launch_fused_prologue(const ModelConst& m, const TraceDev& t, cudaStream_t s);
 void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, uint32_t* d_active,
                   cudaStream_t s);
+void launch_fused_stamp(const TraceDev& t, cudaStream_t s);
 
 }  // namespace tcm
