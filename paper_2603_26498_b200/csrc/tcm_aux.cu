@@ -12,7 +12,7 @@ namespace tcm {
 __global__ void k_init(TraceDev t) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= t.R) return;
-    ReplicaState st;
+    ReplicaState st{};
     st.clock = 0;
     st.kv_free = t.params[r].kv_capacity;
     st.iter = 0;
@@ -32,6 +32,7 @@ __global__ void k_init(TraceDev t) {
     st.sum_pending = 0;
     st.ff_iters = 0;
     st.idle_jumps = 0;
+    st.nlog = 0;
     st.done_count = 0;
     st.scanned = 0;
     t.state[r] = st;

@@ -20,7 +20,8 @@
 // decode calendar keeps, per iteration slot, only the number of finishing requests and the sum
 // of their footprints (updated with fire-and-forget atomics), with its occupancy bitmap in
 // shared memory and a 64-bit word summary in a register.  Finish times are stamped after the
-// launch by k_fstamp from a per-replica log of (iteration, clock) finish events.
+// launch by k_fstamp from a per-replica log of (iteration, clock) events, and so are first-token
+// times: the loop itself never revisits a request once its prefill is complete.
 #include "tcm_internal.cuh"
 #include "tcm_k1.cuh"
 
@@ -30,6 +31,7 @@ namespace {
 
 constexpr uint32_t kThreads = 64;
 constexpr uint64_t kCalFpMask = (1ull << kCalCntShift) - 1;
+constexpr uint64_t kPending = 1ull << 63;
 
 __device__ __forceinline__ void ld_rec(const FRec* p, uint64_t& arr, uint32_t& f, uint32_t& inl, uint32_t& id,
                                        uint32_t& out) {
@@ -38,6 +40,22 @@ __device__ __forceinline__ void ld_rec(const FRec* p, uint64_t& arr, uint32_t& f
     arr = a;
     f = (uint32_t)b;
     inl = (uint32_t)(b >> 32);
+    id = (uint32_t)c;
+    out = (uint32_t)(c >> 32);
+}
+
+// (arrival, footprint, inline) of a record: the first 16 bytes
+__device__ __forceinline__ void ld_rec16(const FRec* p, uint64_t& arr, uint32_t& f, uint32_t& inl) {
+    uint64_t a, b;
+    asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+    arr = a;
+    f = (uint32_t)b;
+    inl = (uint32_t)(b >> 32);
+}
+// (id, out) of a record, usually an L1 hit: its sector came in with ld_rec16
+__device__ __forceinline__ void ld_idout(const FRec* p, uint32_t& id, uint32_t& out) {
+    uint64_t c;
+    asm("ld.global.nc.u64 %0, [%1];" : "=l"(c) : "l"(reinterpret_cast<const char*>(p) + 16));
     id = (uint32_t)c;
     out = (uint32_t)(c >> 32);
 }
@@ -59,39 +77,95 @@ struct Occ {
     __device__ __forceinline__ uint32_t& word(uint32_t i) const { return w[i][tid]; }
 };
 
-// Iteration number of the next occupied calendar slot after `iter` (one exists when n_dec > 0).
-__device__ __forceinline__ uint64_t cal_next(const Occ& o, uint64_t sum, uint64_t iter) {
-    const uint32_t s0 = (uint32_t)((iter + 1) & (kCalSlots - 1));
-    const uint32_t wi = s0 >> 5;
-    uint32_t wv = o.word(wi) & (~0u << (s0 & 31));
-    uint32_t word = wi;
-    if (wv == 0) {
-        const uint64_t rr = rotr64(sum, wi + 1);      // bit k: word (wi + 1 + k) mod 64
-        word = (wi + 1 + (uint32_t)(__ffsll((long long)rr) - 1)) & (kCalWords - 1);
-        wv = o.word(word);
-        if (word == wi) wv &= ~(~0u << (s0 & 31));    // wrapped round to slots before s0
-    }
-    const uint32_t slot = word * 32 + (uint32_t)(__ffs(wv) - 1);
-    return iter + 1 + (uint64_t)((slot - s0) & (kCalSlots - 1));
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Step 9 for iteration `iter` == the next calendar event: every request whose
-// last decode token is produced now completes and releases its KV (R7); the event goes to the
-// log from which k_fstamp stamps their done_us.
-__device__ __forceinline__ void cal_process(const Occ& o, uint64_t& sum, uint64_t* cal, uint64_t* log,
-                                            ReplicaState& st) {
-    const uint32_t s = (uint32_t)(st.iter & (kCalSlots - 1));
-    const unsigned long long v = atomicExch(reinterpret_cast<unsigned long long*>(cal + s), 0ull);
-    const uint32_t cnt = (uint32_t)(v >> kCalCntShift);
-    st.kv_free += v & kCalFpMask;
-    st.n_dec -= cnt;
-    st.done_count += cnt;
+// The decode calendar of one replica.  Slot F & 2047 counts the requests whose last decode
+// token comes in iteration F: (count << 40) | sum of their footprints.  The slot of the next
+// event `next` is held in registers: `pre` (its memory value, loaded as soon as it becomes
+// the next event, so the load overlaps the iterations before it) plus `add` (insertions into
+// it since); other insertions go to memory as fire-and-forget reductions.
+struct Calendar {
+    uint64_t* cal;
+    Occ occ;
+    uint64_t sum;     // bit w: occupancy word w non-zero
+    uint64_t next;    // iteration of the next event (~0: none)
+    uint64_t pre, add;
+
+    // Iteration of the next occupied slot after `iter` (one exists when n_dec > 0).
+    __device__ __forceinline__ uint64_t scan(uint64_t iter) const {
+        const uint32_t s0 = (uint32_t)((iter + 1) & (kCalSlots - 1));
+        const uint32_t wi = s0 >> 5;
+        uint32_t wv = occ.word(wi) & (~0u << (s0 & 31));
+        uint32_t word = wi;
+        if (wv == 0) {
+            const uint64_t rr = rotr64(sum, wi + 1);      // bit k: word (wi + 1 + k) mod 64
+            word = (wi + 1 + (uint32_t)(__ffsll((long long)rr) - 1)) & (kCalWords - 1);
+            wv = occ.word(word);
+            if (word == wi) wv &= ~(~0u << (s0 & 31));    // wrapped round to slots before s0
+        }
+        const uint32_t slot = word * 32 + (uint32_t)(__ffs(wv) - 1);
+        return iter + 1 + (uint64_t)((slot - s0) & (kCalSlots - 1));
+    }
+    __device__ __forceinline__ void find_next(uint64_t iter, uint32_t n_dec) {
+        add = 0;
+        if (n_dec > 0) {
+            next = scan(iter);
+            pre = ld_relaxed(cal + (next & (kCalSlots - 1)));
+        } else {
+            next = ~0ull;
+            pre = 0;
+        }
+    }
+    // A request of footprint f whose last token comes in iteration F (> the current one).
+    __device__ __forceinline__ void insert(uint64_t F, uint32_t f) {
+        const uint64_t v = (1ull << kCalCntShift) | f;
+        const uint32_t s = (uint32_t)(F & (kCalSlots - 1));
+        occ.word(s >> 5) |= 1u << (s & 31);
+        sum |= 1ull << (s >> 5);
+        if (F == next) {
+            add += v;
+        } else if (F < next) {                         // F becomes the next event; slot F is empty
+            if (add) red_add(cal + (next & (kCalSlots - 1)), add);
+            next = F;
+            pre = 0;
+            add = v;
+        } else {
+            red_add(cal + s, v);
+        }
+    }
+    // Step 9 for iteration `next`: every request whose last decode token is
+    // produced now completes and releases its KV (R7).  k_fstamp stamps their done_us from the
+    // event log.
+    __device__ __forceinline__ void process(ReplicaState& st) {
+        const uint32_t s = (uint32_t)(next & (kCalSlots - 1));
+        const uint64_t v = pre + add;
+        if (pre) st_relaxed(cal + s, 0);
+        const uint32_t cnt = (uint32_t)(v >> kCalCntShift);
+        st.kv_free += v & kCalFpMask;
+        st.n_dec -= cnt;
+        uint32_t& w = occ.word(s >> 5);
+        w &= ~(1u << (s & 31));
+        if (w == 0) sum &= ~(1ull << (s >> 5));
+        find_next(st.iter, st.n_dec);
+    }
+    __device__ __forceinline__ void flush() {
+        if (add) red_add(cal + (next & (kCalSlots - 1)), add);
+    }
+};
+
+// One (iteration, clock) entry of the replica's event log: iterations in which a prefill
+// completed or a decode finished, strictly increasing (k_fstamp looks them up).
+__device__ __forceinline__ void log_event(uint64_t* log, ReplicaState& st) {
     asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(log + 2 * (uint64_t)st.nlog), "l"(st.iter),
                  "l"(st.clock) : "memory");
     st.nlog++;
-    uint32_t& w = o.word(s >> 5);
-    w &= ~(1u << (s & 31));
-    if (w == 0) sum &= ~(1ull << (s >> 5));
 }
 
 }  // namespace
@@ -114,8 +188,9 @@ __global__ void k_fpack(ModelConst m, TraceDev t) {
         cnt0 += __popc(__ballot_sync(~0u, q == 0));
         cnt1 += __popc(__ballot_sync(~0u, q == 1));
     }
-    uint32_t run[3] = {0, cnt0, cnt0 + cnt1};
-    FRec* rec = t.fw.rec + a;
+    // segments [0, cnt0) [cnt0 + 1, ..) [.. + 2, ..), each followed by a sentinel record
+    uint32_t run[3] = {0, cnt0 + 1, cnt0 + cnt1 + 2};
+    FRec* rec = t.fw.rec + a + 3ull * r;
     for (uint32_t i0 = 0; i0 < n; i0 += 32) {
         const uint32_t i = i0 + lane;
         int q = 3;
@@ -136,14 +211,15 @@ __global__ void k_fpack(ModelConst m, TraceDev t) {
             run[c] += __popc(b);
         }
     }
+    if (lane < 3) {
+        FRec x{~0ull, 0, 0, 0, 0, 0};
+        rec[run[lane]] = x;                   // sentinel: arrival ~0 never becomes pending
+    }
     if (lane == 0) {
         ReplicaState& st = t.state[r];
         st.head[0] = 0;
-        st.head[1] = cnt0;
-        st.head[2] = cnt0 + cnt1;
-        st.tail[0] = cnt0;                    // segment ends
-        st.tail[1] = cnt0 + cnt1;
-        st.tail[2] = n;
+        st.head[1] = cnt0 + 1;
+        st.head[2] = cnt0 + cnt1 + 2;
     }
 }
 
@@ -159,20 +235,19 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     const uint64_t base = t.offset[r];
     const uint32_t n = (uint32_t)(t.offset[r + 1] - base);
     const uint64_t* __restrict__ arr = t.arrival + base;
-    const FRec* __restrict__ rec = t.fw.rec + base;
-    uint32_t* admit = t.admit_seq + base;
-    uint64_t* first = t.first_token + base;
-    uint64_t* done = t.done + base;
-    uint64_t* fin = t.fw.fin + base;
-    uint64_t* cal = t.fw.cal + (size_t)r * kCalSlots;
-    uint64_t* log = t.fw.log + 2 * base;
-    const Occ occ{occ_s, threadIdx.x};
-    uint64_t osum = 0;
+    const FRec* __restrict__ rec = t.fw.rec + base + 3ull * r;
+    // result / workspace arrays are indexed base + id off the kernel parameters (no per-replica
+    // pointer registers)
+#define admit(i) t.admit_seq[base + (i)]
+#define first(i) t.first_token[base + (i)]
+#define fin(i) t.fw.fin[base + (i)]
+    uint64_t* log = t.fw.log + 4 * base;
+    Calendar cal{t.fw.cal + (size_t)r * kCalSlots, Occ{occ_s, threadIdx.x}, 0, ~0ull, 0, 0};
 #pragma unroll 8
     for (uint32_t k = 0; k < kCalWords; ++k) {
         const uint32_t w = t.occ[(size_t)r * kCalWords + k];
-        occ.word(k) = w;
-        osum |= (uint64_t)(w != 0) << k;
+        cal.occ.word(k) = w;
+        cal.sum |= (uint64_t)(w != 0) << k;
     }
 
     const bool prio = prm.policy == TCM_POLICY_TCM;
@@ -192,25 +267,26 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         return k1_key(kc, w);
     };
 
-    // Register caches: each class queue's head record (arrival, footprint, inline, id) and its
-    // successor's, so that advancing a queue never waits on memory.  An exhausted segment has
-    // arrival ~0: a head is pending iff its arrival <= clock.  st.tail[c] is the end of class
-    // c's segment.
+    // Register caches: each class queue's head record (arrival, footprint, inline) and its
+    // successor's, so that advancing a queue never waits on memory (id / out are read from the
+    // record, in L1, when the head is admitted or completes).  An exhausted segment
+    // ends with a sentinel record of arrival ~0: a head is pending iff its arrival <= clock.
     uint64_t harr[3], sarr[3];
-    uint32_t hf[3], hinl[3], hid[3], sf[3], sinl[3], sid[3];
+    uint32_t hf[3], hinl[3], sf[3], sinl[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const uint32_t h = st.head[c];
-        uint32_t o;
         harr[c] = ~0ull;
-        hf[c] = hinl[c] = hid[c] = 0;
+        hf[c] = hinl[c] = 0;
         sarr[c] = ~0ull;
-        sf[c] = sinl[c] = sid[c] = 0;
-        if (h < st.tail[c]) ld_rec(rec + h, harr[c], hf[c], hinl[c], hid[c], o);
-        if (h + 1 < st.tail[c]) ld_rec(rec + h + 1, sarr[c], sf[c], sinl[c], sid[c], o);
+        sf[c] = sinl[c] = 0;
+        ld_rec16(rec + h, harr[c], hf[c], hinl[c]);
+        if (harr[c] != ~0ull) ld_rec16(rec + h + 1, sarr[c], sf[c], sinl[c]);
     }
+    // next two arrivals in arrival order (a1 counts pending requests)
     uint64_t next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
-    uint64_t next_fin = st.n_dec > 0 ? cal_next(occ, osum, st.iter) : ~0ull;
+    uint64_t next_arr2 = st.nxt + 1 < n ? arr[st.nxt + 1] : ~0ull;
+    cal.find_next(st.iter, st.n_dec);
     uint32_t budget = max_iters;
     bool arm = false;     // the previous decision was blocked: try Lemma L4c once
 
@@ -219,7 +295,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         while (next_arr <= st.clock) {
             st.n_pend++;
             st.nxt++;
-            next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
+            next_arr = next_arr2;
+            next_arr2 = st.nxt + 1 < n ? arr[st.nxt + 1] : ~0ull;
         }
 
         if (st.n_pend == 0) {
@@ -234,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             }
             if (budget == 0) break;
             // ---- Lemma L3: decode-only iterations until the next finish or arrival
-            const uint64_t F = next_fin;
+            const uint64_t F = cal.next;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = F - st.iter;
             if (next_arr != ~0ull) {
@@ -247,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             st.ff_iters += j;
             budget -= (uint32_t)j;
             if (st.iter == F) {
-                cal_process(occ, osum, cal, log, st);
-                next_fin = st.n_dec > 0 ? cal_next(occ, osum, st.iter) : ~0ull;
+                log_event(log, st);
+                cal.process(st);
             }
             continue;
         }
@@ -276,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         if (!stuck && arm && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
             arm = false;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
-            uint64_t j = next_fin - st.iter;
+            uint64_t j = cal.next - st.iter;
             if (next_arr != ~0ull) {
                 const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                 j = ja < j ? ja : j;
@@ -311,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             }
         }
         if (stuck && st.n_dec > 0) {
-            const uint64_t F = next_fin;
+            const uint64_t F = cal.next;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = F - st.iter;
             if (next_arr != ~0ull) {
@@ -327,19 +404,22 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
             budget -= (uint32_t)j;
             if (st.iter == F) {
-                cal_process(occ, osum, cal, log, st);
-                next_fin = st.n_dec > 0 ? cal_next(occ, osum, st.iter) : ~0ull;
+                log_event(log, st);
+                cal.process(st);
             }
             arm = true;                                     // still blocked: try L4c again next
             continue;
         }
 
         // ---- a2 + a3 + a4: merge the class-FIFO heads by key, scan under token/KV budgets.
-        // The scan advances the queue cursors in place; oh[c] keeps each old head for the
-        // first-token walk of a5.
-        uint64_t tok = 0, inl_sum = 0;
+        // The scan advances the queue cursors in place.  A request whose prefill completes gets
+        // its first token in this iteration (R12): its KV release (out = 1) and decode start
+        // are applied after the scan, and its first_token_us / done_us are stamped by k_fstamp
+        // from the iteration number (bit 63 marks it pending) and the event log.
+        uint64_t tok = 0, inl_sum = 0, kv_rel = 0;
+        uint32_t ncomp = 0, new_dec = 0;
+        const uint64_t it1 = st.iter + 1;                   // this iteration's number
         bool blocked = false;                               // R6
-        uint32_t oh[3];
         uint64_t key[3];
         float pf[3];          // FP32 bound of each head's priority (|P~ - P| <= 1e-5)
         bool ex[3];           // ex[c]: key[c] holds the exact K1 key
@@ -350,7 +430,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         };
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            oh[c] = st.head[c];
             key[c] = 0;
             ex[c] = !prio;
             pf[c] = (prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
@@ -358,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         while (left > 0) {
             int best = -1;
             uint64_t bk = 0, ba = 0;
-            uint32_t bi = 0;
+            uint32_t bh = 0;
             float bpf = 0.0f;
             bool bex = true;
 #pragma unroll
@@ -388,7 +467,12 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                                 bex = true;
                             }
                             better = key[c] > bk ||
-                                     (key[c] == bk && (harr[c] < ba || (harr[c] == ba && hid[c] < bi)));
+                                     (key[c] == bk && (harr[c] < ba || (harr[c] == ba && [&] {
+                                         uint32_t ic, ib, o;   // equal key and arrival: id order (R4)
+                                         ld_idout(rec + st.head[c], ic, o);
+                                         ld_idout(rec + bh, ib, o);
+                                         return ic < ib;
+                                     }())));
                         }
                     }
                     if (better) {
@@ -397,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                         bex = ex[c];
                         bpf = pf[c];
                         ba = harr[c];
-                        bi = hid[c];
+                        bh = st.head[c];
                     }
                 }
             }
@@ -412,7 +496,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                             go = false;
                         } else {
                             st.kv_free -= hf[c];            // R7 reserve the full footprint
-                            admit[hid[c]] = st.seq++;
+                            uint32_t id, o;
+                            ld_idout(rec + st.head[c], id, o);
+                            admit(id) = st.seq++;
                             inl_sum += hinl[c];             // R10
                             st.flags |= 1u << c;
                             st.rem[c] = hf[c];
@@ -423,20 +509,29 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                         st.rem[c] -= ch;
                         left -= ch;
                         tok += ch;
-                        if (st.rem[c] == 0) {               // prefill complete: next in FIFO
+                        if (st.rem[c] == 0) {               // prefill complete
+                            uint32_t id, o;
+                            ld_idout(rec + st.head[c], id, o);
+                            first(id) = kPending | it1;
+                            ncomp++;
+                            if (o == 1) {                   // finishes with its first token
+                                fin(id) = it1;
+                                kv_rel += hf[c];
+                            } else {                        // decodes until iteration it1 + out - 1
+                                const uint64_t F = it1 + o - 1;
+                                fin(id) = F;
+                                cal.insert(F, hf[c]);
+                                new_dec++;
+                            }
+                            // next in FIFO
                             st.flags &= ~(1u << c);
                             const uint32_t h = ++st.head[c];
                             harr[c] = sarr[c];
                             hf[c] = sf[c];
                             hinl[c] = sinl[c];
-                            hid[c] = sid[c];
                             ex[c] = !prio;
                             if (prio && harr[c] <= st.clock) pf[c] = bound(c, st.clock - harr[c]);
-                            sarr[c] = ~0ull;
-                            if (h + 1 < st.tail[c]) {
-                                uint32_t o;
-                                ld_rec(rec + h + 1, sarr[c], sf[c], sinl[c], sid[c], o);
-                            }
+                            if (harr[c] != ~0ull) ld_rec16(rec + h + 1, sarr[c], sf[c], sinl[c]);
                         }
                     }
                 }
@@ -451,56 +546,49 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
 
         // ---- a5: iteration cost, clock, decode calendar, first tokens (R12)
         st.clock += m.c0 + m.cp * tok + m.cd * (uint64_t)st.n_dec + inl_sum;
-        st.iter++;
+        st.iter = it1;
         st.decisions++;
         st.scanned++;
         st.sum_pending += st.n_pend;
         st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
         budget--;
-        bool recompute_fin = false;
-        if (st.iter == next_fin) {
-            cal_process(occ, osum, cal, log, st);
-            recompute_fin = true;
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            for (uint32_t k = oh[c]; k < st.head[c]; ++k) {
-                uint64_t a;
-                uint32_t f, il, id, o;
-                ld_rec(rec + k, a, f, il, id, o);
-                first[id] = st.clock;
-                st.n_pend--;
-                if (o == 1) {
-                    done[id] = st.clock;
-                    st.kv_free += f;
-                    st.done_count++;
-                } else {
-                    const uint64_t F = st.iter + o - 1;
-                    const uint32_t s = (uint32_t)(F & (kCalSlots - 1));
-                    red_add(cal + s, (1ull << kCalCntShift) | f);
-                    occ.word(s >> 5) |= 1u << (s & 31);
-                    osum |= 1ull << (s >> 5);
-                    fin[id] = F;
-                    st.n_dec++;
-                    next_fin = F < next_fin ? F : next_fin;
-                }
-            }
-        }
-        if (recompute_fin) next_fin = st.n_dec > 0 ? cal_next(occ, osum, st.iter) : ~0ull;
+        st.n_pend -= ncomp;
+        st.kv_free += kv_rel;
+        st.n_dec += new_dec;
+        const bool event = it1 == cal.next;
+        if (ncomp > 0 || event) log_event(log, st);
+        if (event) cal.process(st);
     }
 
+    st.done_count = st.nxt - st.n_pend - st.n_dec;     // every arrived request is pending, decoding or done
+#undef admit
+#undef first
+#undef fin
     t.state[r] = st;
     if (!(st.flags & FLAG_FINISHED)) {
         atomicAdd(active, 1u);
+        cal.flush();
 #pragma unroll 8
-        for (uint32_t k = 0; k < kCalWords; ++k) t.occ[(size_t)r * kCalWords + k] = occ.word(k);
+        for (uint32_t k = 0; k < kCalWords; ++k) t.occ[(size_t)r * kCalWords + k] = cal.occ.word(k);
     }
 }
 
 // ---------------------------------------------------------------------------------------
-// done_us of every request whose finish iteration F has been reached: the clock of the finish
-// event F, looked up in the replica's event log (sorted by iteration).  One warp per replica,
-// lanes over its requests.
+// first_token_us and done_us from iteration numbers: the clock of iteration I is the entry I of
+// the replica's event log (iterations strictly increasing; every iteration in which a prefill
+// completed or a decode finished has one).  A first token is pending while first_token_us has
+// bit 63 set; a finish while fin != 0, and it is due once the replica's iteration reaches it.
+// One warp per replica, lanes over its requests.
+__device__ __forceinline__ uint64_t log_clock(const uint64_t* log, uint32_t nlog, uint64_t it) {
+    uint32_t lo = 0, hi = nlog;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(log + 2 * mid) <= it) lo = mid;
+        else hi = mid;
+    }
+    return __ldg(log + 2 * lo + 1);
+}
+
 __global__ void k_fstamp(TraceDev t) {
     const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -509,18 +597,15 @@ __global__ void k_fstamp(TraceDev t) {
     const uint32_t n = (uint32_t)(t.offset[r + 1] - a);
     const uint64_t iter = t.state[r].iter;
     const uint32_t nlog = t.state[r].nlog;
-    const uint64_t* log = t.fw.log + 2 * a;
+    const uint64_t* log = t.fw.log + 4 * a;
     for (uint32_t i = lane; i < n; i += 32) {
+        const uint64_t ft = t.first_token[a + i];
+        if (ft & kPending) t.first_token[a + i] = log_clock(log, nlog, ft & ~kPending);
         const uint64_t F = t.fw.fin[a + i];
-        if (F == 0 || F > iter) continue;
-        uint32_t lo = 0, hi = nlog;                        // log[2k] strictly increasing
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(log + 2 * mid) <= F) lo = mid;
-            else hi = mid;
+        if (F != 0 && F <= iter) {
+            t.done[a + i] = log_clock(log, nlog, F);
+            t.fw.fin[a + i] = 0;
         }
-        t.done[a + i] = __ldg(log + 2 * lo + 1);
-        t.fw.fin[a + i] = 0;
     }
 }
 

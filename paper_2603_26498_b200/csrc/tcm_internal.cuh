@@ -37,7 +37,7 @@ struct __align__(16) ReplicaState {
     uint64_t sum_pending;
     uint64_t ff_iters;
     uint32_t idle_jumps;
-    uint32_t nlog;           // fused engine: finish-event log entries (FusedWs::log)
+    uint32_t nlog;           // fused engine: event log entries (FusedWs::log)
     uint32_t done_count;
     uint32_t scanned;        // decisions that ran the full key/merge/scan (not fast-forwarded)
 };
@@ -81,9 +81,9 @@ static_assert(sizeof(FRec) == 32, "FRec is one 32-byte sector");
 
 // Fused engine workspace.
 struct FusedWs {
-    FRec* rec;               // [N] class segments per replica
+    FRec* rec;               // [N + 3R] class segments per replica, each closed by a sentinel
     uint64_t* cal;           // [R * kCalSlots] per iteration slot: (finishing count << 40) | sum of footprints
-    uint64_t* log;           // [2N] per replica (iteration, clock) of every finish event, in order
+    uint64_t* log;           // [4N] per replica (iteration, clock) of every iteration with a first token or a finish
     uint64_t* fin;           // [N] finish iteration of a decoding request (0: none pending)
 };
 constexpr int kCalCntShift = 40;

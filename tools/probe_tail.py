@@ -26,11 +26,12 @@ def timed(gen, params, ncell=32, reps=2):
 
 sw = W.c4(replicas_per_gpu=int(sys.argv[1]) if len(sys.argv) > 1 else 65536)
 R = sw.n_replicas
-ms, st = timed(sw.gen, sw.params)
+only = int(sys.argv[2]) if len(sys.argv) > 2 else -1     # skip straight to this cell's experiments
+ms, st = timed(sw.gen, sw.params) if only < 0 else (0.0, {"decisions": 0, "scanned_decisions": 0})
 print(f"full R={R}: {ms:.1f} ms decisions {st['decisions']:.3e} scanned {st['scanned_decisions']:.3e}", flush=True)
 cells = sw.params["cell_id"]
 per = []
-for c in range(sw.n_cells):
+for c in (range(sw.n_cells) if only < 0 else [only]):
     idx = np.nonzero(cells == c)[0]
     ms, st = timed(sw.gen[idx], sw.params[idx])
     d = sw.cells[c]
