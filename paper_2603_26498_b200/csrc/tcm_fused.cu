@@ -44,20 +44,18 @@ __device__ __forceinline__ void ld_rec(const FRec* p, uint64_t& arr, uint32_t& f
     out = (uint32_t)(c >> 32);
 }
 
-// (arrival, footprint, inline) of a record: the first 16 bytes
-__device__ __forceinline__ void ld_rec16(const FRec* p, uint64_t& arr, uint32_t& f, uint32_t& inl) {
+// (arrival, footprint) of a record
+__device__ __forceinline__ void ld_arrfp(const FRec* p, uint64_t& arr, uint32_t& f) {
     uint64_t a, b;
     asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
     arr = a;
     f = (uint32_t)b;
-    inl = (uint32_t)(b >> 32);
 }
-// (id, out) of a record, usually an L1 hit: its sector came in with ld_rec16
-__device__ __forceinline__ void ld_idout(const FRec* p, uint32_t& id, uint32_t& out) {
-    uint64_t c;
-    asm("ld.global.nc.u64 %0, [%1];" : "=l"(c) : "l"(reinterpret_cast<const char*>(p) + 16));
-    id = (uint32_t)c;
-    out = (uint32_t)(c >> 32);
+// (inline, id, out) of a record, usually an L1 hit: its sector came in with ld_arrfp
+__device__ __forceinline__ void ld_inl_id_out(const FRec* p, uint32_t& inl, uint32_t& id, uint32_t& out) {
+    uint32_t f;
+    asm("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(f), "=r"(inl), "=r"(id), "=r"(out) : "l"(reinterpret_cast<const char*>(p) + 8));
 }
 
 __device__ __forceinline__ void red_add(uint64_t* p, uint64_t v) {
@@ -168,6 +166,19 @@ __device__ __forceinline__ void log_event(uint64_t* log, ReplicaState& st) {
     st.nlog++;
 }
 
+template <class T>
+__device__ __forceinline__ T sel3(int i, const T (&a)[3]) {
+    return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
+}
+
+// Exact K1 key of class c after waiting w, from the replica's class constants.  Out of line:
+// the scan needs it only for heads whose FP32 bounds are within 2.5e-4, and one copy keeps the
+// loop's code small.
+__device__ __noinline__ uint64_t exact_key(const ClassPack* kp, int c, uint64_t w) {
+    const K1Class kc{__ldg(&kp->S[c]), __ldg(&kp->p[c]), __ldg(&kp->C[c]), ((__ldg(&kp->zero_mask) >> c) & 1u) != 0};
+    return k1_key(kc, w);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
@@ -226,10 +237,26 @@ __global__ void k_fpack(ModelConst m, TraceDev t) {
 __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t, uint32_t max_iters,
                                                     uint32_t* active) {
     __shared__ uint32_t occ_s[kCalWords][kThreads];
+    // work counters live in shared memory during the loop (registers are the scarce resource)
+    __shared__ unsigned long long s_dec[kThreads], s_sum[kThreads], s_ff[kThreads];
+    __shared__ uint32_t s_idle[kThreads], s_maxp[kThreads], s_scan[kThreads];
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= t.R) return;
     ReplicaState st = t.state[r];
     if (st.flags & FLAG_FINISHED) return;
+    const uint32_t tid = threadIdx.x;
+    s_dec[tid] = st.decisions;
+    s_sum[tid] = st.sum_pending;
+    s_ff[tid] = st.ff_iters;
+    s_idle[tid] = st.idle_jumps;
+    s_maxp[tid] = st.max_pending;
+    s_scan[tid] = st.scanned;
+    // j decisions with n_pend pending requests each (R17)
+    auto decided = [&](uint64_t j, uint32_t np) {
+        s_dec[tid] += j;
+        s_sum[tid] += j * np;
+        s_maxp[tid] = np > s_maxp[tid] ? np : s_maxp[tid];
+    };
 
     const tcm_replica_params prm = t.params[r];
     const uint64_t base = t.offset[r];
@@ -262,32 +289,36 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     }
     const uint32_t zmask = kp->zero_mask;
     const bool use_bound = kp->filter_ok != 0;   // FP32 bound validated for these constants
-    auto exact_key = [&](int c, uint64_t w) -> uint64_t {
-        const K1Class kc{__ldg(&kp->S[c]), __ldg(&kp->p[c]), __ldg(&kp->C[c]), ((zmask >> c) & 1u) != 0};
-        return k1_key(kc, w);
-    };
 
-    // Register caches: each class queue's head record (arrival, footprint, inline) and its
-    // successor's, so that advancing a queue never waits on memory (id / out are read from the
-    // record, in L1, when the head is admitted or completes).  An exhausted segment
+    // Register caches: each class queue's head (arrival, footprint) and its successor's, so that
+    // advancing a queue never waits on memory (inline / id / out are read from the record, in
+    // L1, when the head is admitted or completes).  An exhausted segment
     // ends with a sentinel record of arrival ~0: a head is pending iff its arrival <= clock.
     uint64_t harr[3], sarr[3];
-    uint32_t hf[3], hinl[3], sf[3], sinl[3];
+    uint32_t hf[3], sf[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const uint32_t h = st.head[c];
         harr[c] = ~0ull;
-        hf[c] = hinl[c] = 0;
+        hf[c] = 0;
         sarr[c] = ~0ull;
-        sf[c] = sinl[c] = 0;
-        ld_rec16(rec + h, harr[c], hf[c], hinl[c]);
-        if (harr[c] != ~0ull) ld_rec16(rec + h + 1, sarr[c], sf[c], sinl[c]);
+        sf[c] = 0;
+        ld_arrfp(rec + h, harr[c], hf[c]);
+        if (harr[c] != ~0ull) ld_arrfp(rec + h + 1, sarr[c], sf[c]);
     }
     // next two arrivals in arrival order (a1 counts pending requests)
     uint64_t next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
     uint64_t next_arr2 = st.nxt + 1 < n ? arr[st.nxt + 1] : ~0ull;
     cal.find_next(st.iter, st.n_dec);
     uint32_t budget = max_iters;
+    // FP32 bound of a head's priority after waiting w (|P~ - P| <= 1e-5)
+    auto bound = [&](int c, uint64_t w) -> float {
+        return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS[c] : k1_filter_f32(fS[c], fp2[c], fC2[c], w);
+    };
+    auto bound_dyn = [&](int c, uint64_t w) -> float {     // c not known at compile time
+        const float S = sel3(c, fS);
+        return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? S : k1_filter_f32(S, sel3(c, fp2), sel3(c, fC2), w);
+    };
     bool arm = false;     // the previous decision was blocked: try Lemma L4c once
 
     for (;;) {
@@ -306,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                     break;
                 }
                 st.clock = next_arr;                    // R15 idle jump (not an iteration)
-                st.idle_jumps++;
+                s_idle[tid]++;
                 continue;
             }
             if (budget == 0) break;
@@ -321,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             j = j < budget ? j : budget;
             st.clock += j * dt;
             st.iter += j;
-            st.ff_iters += j;
+            s_ff[tid] += j;
             budget -= (uint32_t)j;
             if (st.iter == F) {
                 log_event(log, st);
@@ -399,9 +430,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             j = j < l4c_j ? j : l4c_j;
             st.clock += j * dt;
             st.iter += j;
-            st.decisions += j;
-            st.sum_pending += j * st.n_pend;
-            st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
+            decided(j, st.n_pend);
             budget -= (uint32_t)j;
             if (st.iter == F) {
                 log_event(log, st);
@@ -409,6 +438,82 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             }
             arm = true;                                     // still blocked: try L4c again next
             continue;
+        }
+        arm = false;
+
+        // ---- Lemma L5: a partial prefill that outranks every other head able to take tokens
+        // (partial, or waiting and fitting the free KV) and needs more than this iteration's
+        // budget takes the whole budget (a4) while nothing else changes: no admission, no first
+        // token, kv_free and n_dec fixed until the next calendar event, no arrival.  Those
+        // iterations repeat with dt = c0 + cp*Bp + cd*n_dec and are taken in closed form.  Under
+        // TCM the partial's priority now must exceed every other candidate's FP32 bound at the
+        // start of the window's last iteration by 2.5e-4 (priorities only grow, L1); FCFS has
+        // one queue, whose head it is.
+        if (st.flags & 7u) {
+            int top = -1;
+            float ptop = -1.0f;
+            uint32_t cand = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (harr[c] <= st.clock && (((st.flags >> c) & 1u) || (uint64_t)hf[c] <= st.kv_free)) {
+                    cand |= 1u << c;
+                    const float p = prio ? bound(c, st.clock - harr[c]) : 0.0f;
+                    if (top < 0 || p > ptop) {
+                        top = c;
+                        ptop = p;
+                    }
+                }
+            }
+            uint32_t rt = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (c == top) rt = ((st.flags >> c) & 1u) ? st.rem[c] : 0;
+            if (rt > left && (!prio || use_bound)) {
+                const uint64_t dt = m.c0 + m.cp * left + m.cd * st.n_dec;
+                const uint64_t F = cal.next;
+                uint64_t j = (rt - 1) / left;                   // rem stays > 0
+                const uint64_t jf = F - st.iter;
+                j = jf < j ? jf : j;
+                if (next_arr != ~0ull) {
+                    const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+                    j = ja < j ? ja : j;
+                }
+                j = j < budget ? j : budget;
+                cand &= ~(1u << top);
+                bool ok = j >= 1;
+                if (prio && cand) {
+                    ok = false;
+                    for (int h = 0; h < 6 && j >= 1; ++h, j >>= 1) {
+                        const uint64_t t_end = st.clock + (j - 1) * dt;
+                        float pmax = -1.0f;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            if ((cand >> c) & 1u) {
+                                const float p = bound(c, t_end - harr[c]);
+                                pmax = p > pmax ? p : pmax;
+                            }
+                        }
+                        if (ptop - pmax > 2.5e-4f) {
+                            ok = true;
+                            break;
+                        }
+                    }
+                }
+                if (ok) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        if (c == top) st.rem[c] -= (uint32_t)(j * left);
+                    st.clock += j * dt;
+                    st.iter += j;
+                    decided(j, st.n_pend);
+                    budget -= (uint32_t)j;
+                    if (st.iter == F) {
+                        log_event(log, st);
+                        cal.process(st);
+                    }
+                    continue;
+                }
+            }
         }
 
         // ---- a2 + a3 + a4: merge the class-FIFO heads by key, scan under token/KV budgets.
@@ -425,9 +530,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         bool ex[3];           // ex[c]: key[c] holds the exact K1 key
         // Two heads whose bounds are more than 2.5e-4 apart are ordered by the bounds (the exact
         // order, since the bound error is < 1e-5); only closer pairs get their exact FP64 keys.
-        auto bound = [&](int c, uint64_t w) -> float {
-            return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS[c] : k1_filter_f32(fS[c], fp2[c], fC2[c], w);
-        };
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             key[c] = 0;
@@ -452,14 +554,14 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                             better = false;
                         } else {
                             if (!ex[c]) {
-                                key[c] = exact_key(c, st.clock - harr[c]);
+                                key[c] = exact_key(kp, c, st.clock - harr[c]);
                                 ex[c] = true;
                             }
                             if (!bex) {
 #pragma unroll
                                 for (int q = 0; q < c; ++q) {
                                     if (q == best) {
-                                        key[q] = exact_key(q, st.clock - harr[q]);
+                                        key[q] = exact_key(kp, q, st.clock - harr[q]);
                                         ex[q] = true;
                                         bk = key[q];
                                     }
@@ -468,9 +570,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                             }
                             better = key[c] > bk ||
                                      (key[c] == bk && (harr[c] < ba || (harr[c] == ba && [&] {
-                                         uint32_t ic, ib, o;   // equal key and arrival: id order (R4)
-                                         ld_idout(rec + st.head[c], ic, o);
-                                         ld_idout(rec + bh, ib, o);
+                                         uint32_t ic, ib, o, il;   // equal key and arrival: id order (R4)
+                                         ld_inl_id_out(rec + st.head[c], il, ic, o);
+                                         ld_inl_id_out(rec + bh, il, ib, o);
                                          return ic < ib;
                                      }())));
                         }
@@ -486,60 +588,78 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 }
             }
             if (best < 0) break;
+            // the chosen head, with one copy of the code for every class: read its fields,
+            // admit / chunk / complete it, write them back
+            const uint32_t hb = sel3(best, st.head);
+            const uint32_t fb = sel3(best, hf);
+            uint32_t remb = sel3(best, st.rem);
+            bool adv = false;
+            bool go = true;
+            if (!((st.flags >> best) & 1u)) {
+                if ((uint64_t)fb > st.kv_free) {
+                    blocked = true;                         // first misfit stops new admits
+                    go = false;
+                } else {
+                    st.kv_free -= fb;                       // R7 reserve the full footprint
+                    uint32_t il, id, o;
+                    ld_inl_id_out(rec + hb, il, id, o);
+                    admit(id) = st.seq++;
+                    inl_sum += il;                          // R10
+                    st.flags |= 1u << best;
+                    remb = fb;
+                }
+            }
+            if (go) {
+                const uint32_t ch = remb < left ? remb : left;
+                remb -= ch;
+                left -= ch;
+                tok += ch;
+                if (remb == 0) {                            // prefill complete
+                    uint32_t il, id, o;
+                    ld_inl_id_out(rec + hb, il, id, o);
+                    first(id) = kPending | it1;
+                    ncomp++;
+                    if (o == 1) {                           // finishes with its first token
+                        fin(id) = it1;
+                        kv_rel += fb;
+                    } else {                                // decodes until iteration it1 + out - 1
+                        const uint64_t F = it1 + o - 1;
+                        fin(id) = F;
+                        cal.insert(F, fb);
+                        new_dec++;
+                    }
+                    st.flags &= ~(1u << best);
+                    adv = true;
+                }
+            }
+            // next in FIFO: the successor becomes the head, its successor is fetched
+            const uint64_t narr = sel3(best, sarr);
+            float npf = 0.0f;
+            uint64_t s_arr = ~0ull;
+            uint32_t s_f = 0;
+            if (adv) {
+                if (prio && narr <= st.clock) npf = bound_dyn(best, st.clock - narr);
+                if (narr != ~0ull) ld_arrfp(rec + hb + 2, s_arr, s_f);
+            }
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (c == best) {
-                    bool go = true;
-                    if (!((st.flags >> c) & 1u)) {
-                        if ((uint64_t)hf[c] > st.kv_free) {
-                            blocked = true;                 // first misfit stops new admits
-                            go = false;
-                        } else {
-                            st.kv_free -= hf[c];            // R7 reserve the full footprint
-                            uint32_t id, o;
-                            ld_idout(rec + st.head[c], id, o);
-                            admit(id) = st.seq++;
-                            inl_sum += hinl[c];             // R10
-                            st.flags |= 1u << c;
-                            st.rem[c] = hf[c];
-                        }
-                    }
-                    if (go) {
-                        const uint32_t ch = st.rem[c] < left ? st.rem[c] : left;
-                        st.rem[c] -= ch;
-                        left -= ch;
-                        tok += ch;
-                        if (st.rem[c] == 0) {               // prefill complete
-                            uint32_t id, o;
-                            ld_idout(rec + st.head[c], id, o);
-                            first(id) = kPending | it1;
-                            ncomp++;
-                            if (o == 1) {                   // finishes with its first token
-                                fin(id) = it1;
-                                kv_rel += hf[c];
-                            } else {                        // decodes until iteration it1 + out - 1
-                                const uint64_t F = it1 + o - 1;
-                                fin(id) = F;
-                                cal.insert(F, hf[c]);
-                                new_dec++;
-                            }
-                            // next in FIFO
-                            st.flags &= ~(1u << c);
-                            const uint32_t h = ++st.head[c];
-                            harr[c] = sarr[c];
-                            hf[c] = sf[c];
-                            hinl[c] = sinl[c];
-                            ex[c] = !prio;
-                            if (prio && harr[c] <= st.clock) pf[c] = bound(c, st.clock - harr[c]);
-                            if (harr[c] != ~0ull) ld_rec16(rec + h + 1, sarr[c], sf[c], sinl[c]);
-                        }
+                    st.rem[c] = remb;
+                    if (adv) {
+                        st.head[c] = hb + 1;
+                        harr[c] = narr;
+                        hf[c] = sf[c];
+                        ex[c] = !prio;
+                        pf[c] = npf;
+                        sarr[c] = s_arr;
+                        sf[c] = s_f;
                     }
                 }
             }
         }
         arm = tok == 0 && blocked;
         if (tok == 0 && st.n_dec == 0) {                    // unreachable under R6
-            st.status = ST_DEADLOCK;
+            t.state[r].status = ST_DEADLOCK;
             st.flags |= FLAG_FINISHED;
             break;
         }
@@ -547,10 +667,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         // ---- a5: iteration cost, clock, decode calendar, first tokens (R12)
         st.clock += m.c0 + m.cp * tok + m.cd * (uint64_t)st.n_dec + inl_sum;
         st.iter = it1;
-        st.decisions++;
-        st.scanned++;
-        st.sum_pending += st.n_pend;
-        st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
+        decided(1, st.n_pend);
+        s_scan[tid]++;
         budget--;
         st.n_pend -= ncomp;
         st.kv_free += kv_rel;
@@ -564,7 +682,30 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
 #undef admit
 #undef first
 #undef fin
-    t.state[r] = st;
+    {   // write back what the loop changes (tail[] and status are left as they are)
+        ReplicaState& g = t.state[r];
+        g.clock = st.clock;
+        g.kv_free = st.kv_free;
+        g.iter = st.iter;
+        g.nxt = st.nxt;
+        g.seq = st.seq;
+        g.n_dec = st.n_dec;
+        g.n_pend = st.n_pend;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            g.head[c] = st.head[c];
+            g.rem[c] = st.rem[c];
+        }
+        g.flags = st.flags;
+        g.max_pending = s_maxp[tid];
+        g.decisions = s_dec[tid];
+        g.sum_pending = s_sum[tid];
+        g.ff_iters = s_ff[tid];
+        g.idle_jumps = s_idle[tid];
+        g.nlog = st.nlog;
+        g.done_count = st.done_count;
+        g.scanned = s_scan[tid];
+    }
     if (!(st.flags & FLAG_FINISHED)) {
         atomicAdd(active, 1u);
         cal.flush();
