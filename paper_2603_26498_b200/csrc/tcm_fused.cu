@@ -280,13 +280,17 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     const bool prio = prm.policy == TCM_POLICY_TCM;
     const uint32_t B = prm.chunk_budget;
     const ClassPack* kp = t.kpack + r;
-    float fS[3], fp2[3], fC2[3];
+    // FP32 bound constants per class, in shared memory (indexable by a run-time class)
+    __shared__ float s_fc[3][3][kThreads];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        fS[c] = kp->fS[c];
-        fp2[c] = kp->fp2[c];
-        fC2[c] = kp->fC2[c];
+        s_fc[0][c][tid] = kp->fS[c];
+        s_fc[1][c][tid] = kp->fp2[c];
+        s_fc[2][c][tid] = kp->fC2[c];
     }
+#define fS(c) s_fc[0][c][tid]
+#define fp2(c) s_fc[1][c][tid]
+#define fC2(c) s_fc[2][c][tid]
     const uint32_t zmask = kp->zero_mask;
     const bool use_bound = kp->filter_ok != 0;   // FP32 bound validated for these constants
 
@@ -313,11 +317,10 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     uint32_t budget = max_iters;
     // FP32 bound of a head's priority after waiting w (|P~ - P| <= 1e-5)
     auto bound = [&](int c, uint64_t w) -> float {
-        return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS[c] : k1_filter_f32(fS[c], fp2[c], fC2[c], w);
+        return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS(c) : k1_filter_f32(fS(c), fp2(c), fC2(c), w);
     };
     auto bound_dyn = [&](int c, uint64_t w) -> float {     // c not known at compile time
-        const float S = sel3(c, fS);
-        return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? S : k1_filter_f32(S, sel3(c, fp2), sel3(c, fC2), w);
+        return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS(c) : k1_filter_f32(fS(c), fp2(c), fC2(c), w);
     };
     bool arm = false;     // the previous decision was blocked: try Lemma L4c once
 
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 const bool pend = harr[c] <= st.clock;
                 zero_head |= pend && ((zmask >> c) & 1u);
                 if (pend && !((zmask >> c) & 1u) && (uint64_t)hf[c] > st.kv_free) {
-                    const float p = k1_filter_f32(fS[c], fp2[c], fC2[c], st.clock - harr[c]);
+                    const float p = k1_filter_f32(fS(c), fp2(c), fC2(c), st.clock - harr[c]);
                     ptop = p > ptop ? p : ptop;
                 }
             }
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     if (harr[c] <= st.clock && (uint64_t)hf[c] <= st.kv_free) {
-                        const float p = k1_filter_f32(fS[c], fp2[c], fC2[c], t_end - harr[c]);
+                        const float p = k1_filter_f32(fS(c), fp2(c), fC2(c), t_end - harr[c]);
                         pfit = p > pfit ? p : pfit;
                     }
                 }
@@ -679,6 +682,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     }
 
     st.done_count = st.nxt - st.n_pend - st.n_dec;     // every arrived request is pending, decoding or done
+#undef fS
+#undef fp2
+#undef fC2
 #undef admit
 #undef first
 #undef fin
