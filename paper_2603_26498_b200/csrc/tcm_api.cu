@@ -112,7 +112,7 @@ size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) 
         b += (size_t)R * kCalSlots * 4;          // calendar slot list heads
     } else {
         b += (sizeof(FRec) + 32 + 8) * N;        // class-segment records, event log, finish iterations
-        b += sizeof(FRec) * 3ull * R;            // segment sentinels
+        b += sizeof(FRec) * 6ull * R;            // segment sentinels
         b += (size_t)R * kCalSlots * 8;          // calendar slot counters
     }
     b += (size_t)R * kCalWords * 4;              // occupancy
@@ -297,7 +297,7 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         if ((st = dalloc(c, &p, (size_t)R * kCalSlots * 4))) return st;
         t.cal = (uint32_t*)p;
     } else {
-        if ((st = dalloc(c, &p, sizeof(FRec) * (N + 3ull * R)))) return st;
+        if ((st = dalloc(c, &p, sizeof(FRec) * (N + 6ull * R)))) return st;
         t.fw.rec = (FRec*)p;
         if ((st = dalloc(c, &p, 32 * N))) return st;
         t.fw.log = (uint64_t*)p;

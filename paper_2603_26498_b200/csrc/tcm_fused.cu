@@ -51,6 +51,21 @@ __device__ __forceinline__ void ld_arrfp(const FRec* p, uint64_t& arr, uint32_t&
     arr = a;
     f = (uint32_t)b;
 }
+// Asynchronous 16-byte copy global -> shared (its own commit group).  `dep` is an unused operand
+// that makes the copy wait for a register (the value just read from the same shared slot).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t dep) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("{\n\t.reg .b64 d;\n\tmov.b64 d, %2;\n\tcp.async.cg.shared.global [%0], [%1], 16;\n\t"
+                 "cp.async.commit_group;\n\t}" ::"r"(sa), "l"(gmem), "l"(dep) : "memory");
+}
+// Wait until at most `newer` of this thread's most recent copy groups are still in flight.
+__device__ __forceinline__ void cp_async_wait(uint32_t newer) {
+    if (newer == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    else if (newer == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else if (newer == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else asm volatile("cp.async.wait_group 3;" ::: "memory");
+}
+
 // (inline, id, out) of a record, usually an L1 hit: its sector came in with ld_arrfp
 __device__ __forceinline__ void ld_inl_id_out(const FRec* p, uint32_t& inl, uint32_t& id, uint32_t& out) {
     uint32_t f;
@@ -199,9 +214,9 @@ __global__ void k_fpack(ModelConst m, TraceDev t) {
         cnt0 += __popc(__ballot_sync(~0u, q == 0));
         cnt1 += __popc(__ballot_sync(~0u, q == 1));
     }
-    // segments [0, cnt0) [cnt0 + 1, ..) [.. + 2, ..), each followed by a sentinel record
-    uint32_t run[3] = {0, cnt0 + 1, cnt0 + cnt1 + 2};
-    FRec* rec = t.fw.rec + a + 3ull * r;
+    // segments [0, cnt0) [cnt0 + 2, ..) [.. + 4, ..), each followed by two sentinel records
+    uint32_t run[3] = {0, cnt0 + 2, cnt0 + cnt1 + 4};
+    FRec* rec = t.fw.rec + a + 6ull * r;
     for (uint32_t i0 = 0; i0 < n; i0 += 32) {
         const uint32_t i = i0 + lane;
         int q = 3;
@@ -222,15 +237,15 @@ __global__ void k_fpack(ModelConst m, TraceDev t) {
             run[c] += __popc(b);
         }
     }
-    if (lane < 3) {
+    if (lane < 6) {
         FRec x{~0ull, 0, 0, 0, 0, 0};
-        rec[run[lane]] = x;                   // sentinel: arrival ~0 never becomes pending
+        rec[run[lane >> 1] + (lane & 1)] = x;   // sentinels: arrival ~0 never becomes pending
     }
     if (lane == 0) {
         ReplicaState& st = t.state[r];
         st.head[0] = 0;
-        st.head[1] = cnt0 + 1;
-        st.head[2] = cnt0 + cnt1 + 2;
+        st.head[1] = cnt0 + 2;
+        st.head[2] = cnt0 + cnt1 + 4;
     }
 }
 
@@ -262,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     const uint64_t base = t.offset[r];
     const uint32_t n = (uint32_t)(t.offset[r + 1] - base);
     const uint64_t* __restrict__ arr = t.arrival + base;
-    const FRec* __restrict__ rec = t.fw.rec + base + 3ull * r;
+    const FRec* __restrict__ rec = t.fw.rec + base + 6ull * r;
     // result / workspace arrays are indexed base + id off the kernel parameters (no per-replica
     // pointer registers)
 #define admit(i) t.admit_seq[base + (i)]
@@ -298,17 +313,27 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     // advancing a queue never waits on memory (inline / id / out are read from the record, in
     // L1, when the head is admitted or completes).  An exhausted segment
     // ends with a sentinel record of arrival ~0: a head is pending iff its arrival <= clock.
-    uint64_t harr[3], sarr[3];
-    uint32_t hf[3], sf[3];
+    uint64_t harr[3];
+    uint32_t hf[3];
+    // the next two records of each class queue, (arrival, footprint | inline << 32), prefetched
+    // into shared memory by cp.async: slot k & 1 holds record k
+    __shared__ ulonglong2 s_ring[3][2][kThreads];
+    __shared__ uint32_t s_gseq[3][2][kThreads];           // commit-group number of each slot's copy
+    uint32_t ng = 0;                                       // copy groups committed so far
+    auto prefetch = [&](int c, uint32_t k, uint64_t dep) {
+        cp_async16(&s_ring[c][k & 1][tid], rec + k, dep);
+        s_gseq[c][k & 1][tid] = ng++;
+    };
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const uint32_t h = st.head[c];
         harr[c] = ~0ull;
         hf[c] = 0;
-        sarr[c] = ~0ull;
-        sf[c] = 0;
         ld_arrfp(rec + h, harr[c], hf[c]);
-        if (harr[c] != ~0ull) ld_arrfp(rec + h + 1, sarr[c], sf[c]);
+        if (harr[c] != ~0ull) {
+            prefetch(c, h + 1, 0);
+            prefetch(c, h + 2, 0);
+        }
     }
     // next two arrivals in arrival order (a1 counts pending requests)
     uint64_t next_arr = st.nxt < n ? arr[st.nxt] : ~0ull;
@@ -635,14 +660,19 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                     adv = true;
                 }
             }
-            // next in FIFO: the successor becomes the head, its successor is fetched
-            const uint64_t narr = sel3(best, sarr);
+            // next in FIFO: the prefetched successor becomes the head, the record after the new
+            // successor is prefetched into the slot it leaves
+            uint64_t narr = ~0ull;
+            uint32_t nf = 0;
             float npf = 0.0f;
-            uint64_t s_arr = ~0ull;
-            uint32_t s_f = 0;
             if (adv) {
+                const uint32_t sl = (hb + 1) & 1;
+                cp_async_wait(ng - 1 - s_gseq[best][sl][tid]);
+                const ulonglong2 v = s_ring[best][sl][tid];
+                narr = v.x;
+                nf = (uint32_t)v.y;
+                if (narr != ~0ull) prefetch(best, hb + 3, narr);
                 if (prio && narr <= st.clock) npf = bound_dyn(best, st.clock - narr);
-                if (narr != ~0ull) ld_arrfp(rec + hb + 2, s_arr, s_f);
             }
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -651,11 +681,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                     if (adv) {
                         st.head[c] = hb + 1;
                         harr[c] = narr;
-                        hf[c] = sf[c];
+                        hf[c] = nf;
                         ex[c] = !prio;
                         pf[c] = npf;
-                        sarr[c] = s_arr;
-                        sf[c] = s_f;
                     }
                 }
             }
@@ -681,6 +709,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         if (event) cal.process(st);
     }
 
+    asm volatile("cp.async.wait_all;" ::: "memory");
     st.done_count = st.nxt - st.n_pend - st.n_dec;     // every arrived request is pending, decoding or done
 #undef fS
 #undef fp2

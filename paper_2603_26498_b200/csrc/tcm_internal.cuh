@@ -81,7 +81,7 @@ static_assert(sizeof(FRec) == 32, "FRec is one 32-byte sector");
 
 // Fused engine workspace.
 struct FusedWs {
-    FRec* rec;               // [N + 3R] class segments per replica, each closed by a sentinel
+    FRec* rec;               // [N + 6R] class segments per replica, each closed by two sentinels
     uint64_t* cal;           // [R * kCalSlots] per iteration slot: (finishing count << 40) | sum of footprints
     uint64_t* log;           // [4N] per replica (iteration, clock) of every iteration with a first token or a finish
     uint64_t* fin;           // [N] finish iteration of a decoding request (0: none pending)
