@@ -31,9 +31,11 @@ sys.path.insert(0, ROOT)
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0           # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
 
-# algorithmic bytes: fused engine per simulated request / per replica
-FUSED_BYTES_PER_REQ = 19 + 20 + 8 + 8     # trace read, results written, FIFO link w+r, calendar push+pop
-FUSED_BYTES_PER_REPLICA = 256 + 8192 + 256  # state r+w, calendar heads init, occupancy
+# algorithmic bytes of k_fused per simulated request: class record read (32), arrival
+# stream (8), admit_seq (4), first-token iteration (8), finish iteration (8), calendar slot
+# reduction (8), event-log entry (16); per replica: state r+w, class constants, params, occupancy
+FUSED_BYTES_PER_REQ = 32 + 8 + 4 + 8 + 8 + 8 + 16
+FUSED_BYTES_PER_REPLICA = 256 + 144 + 32 + 256
 STEP_BYTES_PER_PENDING = 9                 # stepwise: arrival (8) + state byte (1) per pending key
 STEP_BYTES_PER_DECISION = 256              # replica state r+w
 
@@ -209,11 +211,14 @@ def run_tcm(args, rank, world, local):
         e0.record(stream)
         sim.run()
         e1.record(stream)
-        tcm.tcm_stats(sim.ctx, hist, cnt)
+        st = tcm.tcm_stats(sim.ctx, hist, cnt)
         if dist is not None:
             with torch.cuda.stream(stream):
                 W.allreduce_aggregate(hist, cnt)      # int64 SUM over NVLink (NCCL)
+        kms.append((st["reset_ms"], st["engine_ms"], st["stamp_ms"]))
         return e0, e1
+
+    kms = []     # per step: library-recorded device ms of (reset + prologue, k_fused, k_fstamp)
 
     for _ in range(args.warmup):
         one_step()
@@ -229,6 +234,7 @@ def run_tcm(args, rank, world, local):
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     kern = []
+    kms.clear()
     for _ in range(args.steps):
         kern.append(one_step())
     t_end.record(stream)
@@ -254,11 +260,12 @@ def run_tcm(args, rank, world, local):
     req_s = float(tot[0]) / (ms_max / 1e3)
     dec_s = float(tot[1]) / (ms_max / 1e3)
 
-    # roofline of the dominant kernel (k_fused): algorithmic bytes per launch / launch time
+    # roofline of the dominant kernel (k_fused): algorithmic bytes per launch / its launch time,
+    # from CUDA events the library records around the launch on this stream
     peak, peak_kind = peak_hbm()
-    run_avg_ms = float(np.mean(run_ms))
+    fused_ms = float(np.mean([k[1] for k in kms]))
     alg_bytes = N * FUSED_BYTES_PER_REQ + R * FUSED_BYTES_PER_REPLICA
-    achieved = alg_bytes / (run_avg_ms / 1e3) / 1e9
+    achieved = alg_bytes / (fused_ms / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "fused_dram_bytes.json")
     if os.path.exists(prof):
@@ -281,7 +288,10 @@ def run_tcm(args, rank, world, local):
                    "l2": "inputs larger than L2 (trace %.1f GB per GPU)" % (N * 19 / 1e9)},
         "roofline": {"kernel": "k_fused", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "launch_ms": fused_ms, "alg_bytes_per_launch": alg_bytes,
                      "note": "latency-bound per-replica chains; HBM is not the binding roof (DESIGN.md 7)"},
+        "kernel_ms_per_step": {"reset_and_prologue": float(np.mean([k[0] for k in kms])), "k_fused": fused_ms,
+                               "k_fstamp": float(np.mean([k[2] for k in kms]))},
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clocks,
         "work": {"iterations_per_step": st1["iterations"], "decisions_per_step": st1["decisions"],

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define TCM_ABI_VERSION 1u
+#define TCM_ABI_VERSION 2u
 
 typedef int32_t tcm_status;
 #define TCM_OK 0
@@ -146,6 +146,13 @@ typedef struct tcm_stats_host {
                                    were taken in closed form, Lemma L4)  */
     int32_t first_bad_replica; /* -1 if none                                          */
     int32_t first_bad_status;
+    /* Device time (ms) since the last tcm_load_trace / tcm_reset, from CUDA events recorded
+     * on the context's stream around the library's own launches:                          */
+    double reset_ms;           /* the reset: memsets, state init, engine prologue (FUSED: the
+                                  class-segment build, row a1)                            */
+    double engine_ms;          /* the step kernels (FUSED: k_fused; STEPWISE: all of its
+                                  per-iteration kernels)                                   */
+    double stamp_ms;           /* FUSED: k_fstamp (first-token / finish times from the log) */
 } tcm_stats_host;
 
 typedef struct tcm_ctx tcm_ctx;

@@ -23,7 +23,8 @@ struct tcm_ctx {
     std::string err;
     bool loaded = false;
     TraceDev t{};
-    std::vector<void*> allocs;           // workspace + HOST mirrors, freed on reload/destroy
+    std::vector<std::pair<void*, size_t>> allocs;   // workspace + HOST mirrors
+    std::vector<std::pair<void*, size_t>> spare;    // the previous trace's, reused by size on reload
     bool host_results = false;
     tcm_results_view host_res{};
     uint32_t* d_active = nullptr;        // [1]
@@ -31,6 +32,10 @@ struct tcm_ctx {
     uint32_t* d_val = nullptr;           // [2]
     StepwiseWorkspace sw{};
     uint64_t launches = 0;
+    // device timing of the library's launches (tcm_stats_host.*_ms)
+    cudaEvent_t ev[5] = {};              // reset begin/end, engine begin/end, stamp end
+    bool reset_pending = false;          // ev[0..1] recorded, not yet read
+    double reset_ms = 0, engine_ms = 0, stamp_ms = 0;
 };
 
 namespace {
@@ -55,21 +60,44 @@ tcm_status fail(tcm_ctx* c, tcm_status code, const char* fmt, ...) {
             return fail((ctx), TCM_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));    \
     } while (0)
 
-void free_allocs(tcm_ctx* c) {
-    for (void* p : c->allocs) cudaFree(p);
+// keep: park the buffers for reuse by the next tcm_load_trace (reloading a trace of the same
+// shape then allocates nothing); otherwise free everything.
+void free_allocs(tcm_ctx* c, bool keep = false) {
+    for (auto& a : c->allocs) {
+        if (keep) c->spare.push_back(a);
+        else cudaFree(a.first);
+    }
     c->allocs.clear();
+    if (!keep) {
+        for (auto& a : c->spare) cudaFree(a.first);
+        c->spare.clear();
+    }
     c->loaded = false;
     c->sw = StepwiseWorkspace{};
 }
 
 tcm_status dalloc(tcm_ctx* c, void** p, size_t bytes) {
     if (bytes == 0) bytes = 16;
+    for (size_t i = 0; i < c->spare.size(); ++i) {
+        if (c->spare[i].second == bytes) {
+            *p = c->spare[i].first;
+            c->spare.erase(c->spare.begin() + i);
+            c->allocs.push_back({*p, bytes});
+            return TCM_OK;
+        }
+    }
     cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess && !c->spare.empty()) {      // the parked buffers may be in the way
+        cudaGetLastError();
+        for (auto& a : c->spare) cudaFree(a.first);
+        c->spare.clear();
+        e = cudaMalloc(p, bytes);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(c, TCM_E_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
     }
-    c->allocs.push_back(*p);
+    c->allocs.push_back({*p, bytes});
     return TCM_OK;
 }
 
@@ -151,6 +179,8 @@ tcm_status reduce_stats(tcm_ctx* c, unsigned long long* h) {
 tcm_status reset_state(tcm_ctx* c) {
     const TraceDev& t = c->t;
     cudaStream_t s = c->s;
+    c->reset_ms = c->engine_ms = c->stamp_ms = 0;
+    TCM_CUDA(c, cudaEventRecord(c->ev[0], s));
     const uint32_t R = t.R;
     const uint64_t N = t.N;
     if (t.cal) TCM_CUDA(c, cudaMemsetAsync(t.cal, 0xFF, (size_t)R * kCalSlots * 4, s));
@@ -171,13 +201,17 @@ tcm_status reset_state(tcm_ctx* c) {
         c->launches++;
     }
     TCM_CUDA(c, cudaGetLastError());
+    TCM_CUDA(c, cudaEventRecord(c->ev[1], s));
+    c->reset_pending = true;
     return TCM_OK;
 }
 
 tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
     TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
+    TCM_CUDA(c, cudaEventRecord(c->ev[2], c->s));
     if (c->cfg.engine == TCM_ENGINE_FUSED) {
         launch_fused(c->m, c->t, max_iters, c->d_active, c->s);
+        TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
         launch_fused_stamp(c->t, c->s);
         c->launches += 2;
     } else {
@@ -187,8 +221,20 @@ tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
         if (st != TCM_OK) return fail(c, st, "stepwise engine failed: %s", cudaGetErrorString(cudaGetLastError()));
     }
     TCM_CUDA(c, cudaGetLastError());
+    if (c->cfg.engine != TCM_ENGINE_FUSED) TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
+    TCM_CUDA(c, cudaEventRecord(c->ev[4], c->s));
     TCM_CUDA(c, cudaMemcpyAsync(active, c->d_active, 4, cudaMemcpyDeviceToHost, c->s));
     TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    float ms = 0;
+    if (c->reset_pending) {
+        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+        c->reset_ms += ms;
+        c->reset_pending = false;
+    }
+    TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+    c->engine_ms += ms;
+    TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
+    c->stamp_ms += ms;
     return TCM_OK;
 }
 
@@ -210,11 +256,14 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
     if (e == cudaSuccess) e = cudaMalloc(&c->d_active, 4);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_acc, kAccN * 8);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 8);
+    for (int i = 0; i < 5 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     if (e != cudaSuccess) {
         fail(nullptr, TCM_E_CUDA, "tcm_create: %s", cudaGetErrorString(e));
         cudaFree(c->d_active);
         cudaFree(c->d_acc);
         cudaFree(c->d_val);
+        for (auto& ev : c->ev)
+            if (ev) cudaEventDestroy(ev);
         delete c;
         return TCM_E_CUDA;
     }
@@ -230,7 +279,7 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         !tv->inline_us || !tv->out_tokens || !tv->modality)))
         return fail(c, TCM_E_ARG, "trace arrays must be non-NULL");
     if (tv->mem > TCM_MEM_HOST || (rv && rv->mem > TCM_MEM_HOST)) return fail(c, TCM_E_ARG, "bad mem kind");
-    free_allocs(c);
+    free_allocs(c, true);
     const uint32_t R = tv->n_replicas;
     const uint64_t N = tv->n_requests;
     TraceDev t{};
@@ -345,6 +394,8 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         tcm_status rs = reset_state(c);
         if (rs != TCM_OK) return rs;
     }
+    for (auto& a : c->spare) cudaFree(a.first);     // what this trace did not reuse
+    c->spare.clear();
     c->loaded = true;
     c->err.clear();
     return TCM_OK;
@@ -406,6 +457,15 @@ tcm_status tcm_stats(tcm_ctx* c, tcm_stats_host* out, int64_t* dev_hist, int64_t
         out->scanned_decisions = h[kAccScanned];
         out->first_bad_replica = h[kAccBadStatus] ? (int32_t)h[kAccBadReplica] : -1;
         out->first_bad_status = (int32_t)h[kAccBadStatus];
+        if (c->reset_pending) {
+            float ms = 0;
+            TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+            c->reset_ms += ms;
+            c->reset_pending = false;
+        }
+        out->reset_ms = c->reset_ms;
+        out->engine_ms = c->engine_ms;
+        out->stamp_ms = c->stamp_ms;
     }
     if (dev_hist || dev_cnt) {
         if (h[kAccReplicasActive] != 0)
@@ -429,6 +489,8 @@ tcm_status tcm_stats(tcm_ctx* c, tcm_stats_host* out, int64_t* dev_hist, int64_t
 void tcm_destroy(tcm_ctx* c) {
     if (!c) return;
     free_allocs(c);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
     cudaFree(c->d_active);
     cudaFree(c->d_acc);
     cudaFree(c->d_val);

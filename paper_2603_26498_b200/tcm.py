@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_build", "libtcm.so")
 
-TCM_ABI_VERSION = 1
+TCM_ABI_VERSION = 2
 TCM_OK = 0
 ERRORS = {-1: "TCM_E_ARG", -2: "TCM_E_STATE", -3: "TCM_E_CAPACITY", -4: "TCM_E_CUDA",
           -5: "TCM_E_OOM", -6: "TCM_E_REPLICA", -7: "TCM_E_VERSION"}
@@ -68,7 +68,8 @@ class tcm_stats_host(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "iterations", "decisions", "ff_iterations", "idle_jumps", "sum_pending", "max_pending",
         "requests_done", "replicas_done", "replicas_active", "kernel_launches", "scanned_decisions")] + [
-        ("first_bad_replica", ctypes.c_int32), ("first_bad_status", ctypes.c_int32)]
+        ("first_bad_replica", ctypes.c_int32), ("first_bad_status", ctypes.c_int32),
+        ("reset_ms", ctypes.c_double), ("engine_ms", ctypes.c_double), ("stamp_ms", ctypes.c_double)]
 
 
 # tcm_replica_params (32 B) as a numpy record so whole sweeps are built vectorised.
