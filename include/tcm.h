@@ -143,7 +143,7 @@ typedef struct tcm_stats_host {
     uint64_t replicas_active;
     uint64_t kernel_launches;  /* library kernels launched since tcm_create          */
     uint64_t scanned_decisions; /* decisions that ran the full key/order/scan (the rest
-                                   were taken in closed form, Lemma L4)  */
+                                   were taken in closed form, Lemmas L4-L5) */
     int32_t first_bad_replica; /* -1 if none                                          */
     int32_t first_bad_status;
     /* Device time (ms) since the last tcm_load_trace / tcm_reset, from CUDA events recorded

@@ -88,8 +88,9 @@ def main():
     m = ms[0]
     dur = to_float(m["gpu__time_duration.sum"][0])
     dur_unit = m["gpu__time_duration.sum"][1]
-    rd, rdu = to_float(m["dram__bytes_read.sum"][0]), m["dram__bytes_read.sum"][1]
-    wr, wru = to_float(m["dram__bytes_write.sum"][0]), m["dram__bytes_write.sum"][1]
+    nob = ("0", "byte")          # a capture without the memory sections has no DRAM byte counts
+    rd, rdu = to_float(m.get("dram__bytes_read.sum", nob)[0]), m.get("dram__bytes_read.sum", nob)[1]
+    wr, wru = to_float(m.get("dram__bytes_write.sum", nob)[0]), m.get("dram__bytes_write.sum", nob)[1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
     traffic = rd * scale.get(rdu, 1) + wr * scale.get(wru, 1)
@@ -104,8 +105,9 @@ def main():
     with open(a.out + ".md", "w") as f:
         f.write(f"# ncu --set full: {m['kernel']}\n\n{a.note}\n\n")
         f.write(f"- duration: {secs * 1e3:.3f} ms (cold-cache, serialised replay)\n")
-        f.write(f"- DRAM traffic: {traffic / 1e6:.1f} MB ({traffic / secs / 1e9:.1f} GB/s)\n")
-        if a.alg_bytes:
+        if traffic:
+            f.write(f"- DRAM traffic: {traffic / 1e6:.1f} MB ({traffic / secs / 1e9:.1f} GB/s)\n")
+        if a.alg_bytes and traffic:
             f.write(f"- algorithmic bytes: {a.alg_bytes / 1e6:.1f} MB (traffic / algorithmic = {traffic / a.alg_bytes:.2f})\n")
         f.write("\n| metric | value | unit |\n|---|---|---|\n")
         for k, (v, u) in summary["metrics"].items():
