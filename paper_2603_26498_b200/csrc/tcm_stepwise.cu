@@ -339,13 +339,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             // after the current 32nd, using S_c <= P <= S_c + 1 exactly.
             uint64_t lk = 0, kk = 0;
             uint32_t li = NIL, ki = NIL;
-            // threshold state derived from the warp's current 32nd (kk, ki): a float lower bound
-            // of its priority and the classes whose exact cap S_c <= P <= Smax_c rules them out
-            float thrf = 0.0f;
+            // threshold state derived from the warp's current 32nd (kk, ki).  Lean path: per
+            // class c an arrival limit amax[c] such that every class-c request arriving after it
+            // provably ranks after (kk, ki); a request is queued for its exact key only if
+            // arrival <= amax[c].  Derivation: K1 is non-decreasing in w (Lemma L1's
+            // premise, audited on [0, 2^33) us), so for w <= W-1, P(w) <= P(W-1) <= P~(W-1) + 1e-5;
+            // one FP32 bound evaluation at W-1 with fadd_ru(P~, 1e-4) < rd(P(kk)) proves it for the
+            // whole class.  Classes whose exact cap is below (or ties) P(kk) are excluded outright
+            // (a tie loses on id: every chunk this warp streams after (kk, ki) entered its list holds
+            // larger ids than every list entry, ki < e).
+            const bool lean = prio && filter_ok && !has_th;    // FP32-bound path (else: exact for all)
+            const bool lean_path = lean;
             uint32_t skipm = 0, tiem = 0;
+            int64_t am0 = INT64_MAX, am1 = INT64_MAX, am2 = INT64_MAX, amx = INT64_MAX;   // amx = max_c am_c
             auto retune = [&]() {
                 const double Pkk = __longlong_as_double((long long)kk);
-                thrf = __double2float_rd(Pkk);
+                const float thrf = __double2float_rd(Pkk);
                 skipm = 0;
                 tiem = 0;
 #pragma unroll
@@ -354,6 +363,36 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     if (cap < Pkk) skipm |= 1u << c;
                     else if (cap == Pkk) tiem |= 1u << c;
                 }
+                if (!lean_path) return;
+                int64_t am = INT64_MAX;
+                const int c = lane;
+                if (c < 3) {
+                    if ((skipm | tiem) >> c & 1u) {
+                        am = -1;
+                    } else if (!((zero_mask >> c) & 1u)) {
+                        const float fS = sm.kp.fS[c], p2 = sm.kp.fp2[c], C2 = sm.kp.fC2[c];
+                        const float d = thrf - fS - 3e-4f;
+                        uint64_t W = 0;
+                        if (d > 0.0f && d < 1.0f) {
+                            // estimate: P~(w) = S + 1 - e^-x, x = 2^(p2 log2 w + C2)
+                            const float x = -sfu_lg2(1.0f - d) * 0.693147182f;
+                            const float L = (sfu_lg2(x) - C2) / p2;
+                            W = L >= 62.0f ? (1ull << 62) : (L <= 1.0f ? 0ull : __float2ull_rd(sfu_ex2(L)));
+                            for (int tr = 0; tr < 3 && W >= 2; ++tr) {
+                                const float pf = k1_filter_f32(fS, p2, C2, W - 1);
+                                if (__fadd_ru(pf, 1e-4f) < thrf) break;
+                                W = tr < 2 ? W - (W >> 3) : 0;
+                            }
+                            if (W < 2) W = 0;
+                        }
+                        am = W > clock ? -1 : (int64_t)(clock - W);
+                    }
+                }
+                am0 = __shfl_sync(0xFFFFFFFFu, am, 0);
+                am1 = __shfl_sync(0xFFFFFFFFu, am, 1);
+                am2 = __shfl_sync(0xFFFFFFFFu, am, 2);
+                amx = am0 > am1 ? am0 : am1;
+                amx = amx > am2 ? amx : am2;
             };
             int qn = 0;
             uint32_t* qid = sm.qid[wg];
@@ -362,8 +401,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             auto take = [&](uint64_t key, uint32_t id, bool enter) {   // warp-collective
                 const uint32_t em = __ballot_sync(0xFFFFFFFFu, enter);
                 if (em == 0) return;
-                if (__popc(em) <= 6) {
-                    // few entrants: insert each into the sorted list (rank by ballot, shift by shuffle)
+                if (__popc(em) <= 16) {
+                    // up to 16 entrants: insert each into the sorted list (rank by ballot, shift by shuffle)
                     uint32_t rest = em;
                     while (rest) {
                         const int src = __ffs(rest) - 1;
@@ -398,11 +437,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 uint64_t key = 0;
                 uint32_t id = NIL;
                 bool enter = false;
+                bool live = false;
+                int cc = 0;
+                uint64_t qwl = 0;
                 if (lane < cnt) {
                     id = qid[lane];
-                    const int cc = qc[lane];
+                    cc = qc[lane];
+                    qwl = qw[lane];
+                    // the limits may have tightened since this request was queued.  The queue is
+                    // not in id order within a chunk, so a tie class is decided by id here.
+                    const int qcl = cc & RS_CLS;
+                    const int64_t am = qcl == 0 ? am0 : (qcl == 1 ? am1 : am2);
+                    live = !lean_path || (first_pass && (cc & RS_RES)) ||
+                           (((tiem >> qcl) & 1u) ? id < ki : (int64_t)(clock - qwl) <= am);
+                }
+                if (!__any_sync(0xFFFFFFFFu, live)) return;
+                if (live) {
                     const int c = cc & RS_CLS;
-                    key = prio ? k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qw[lane], tb) : 0;
+                    key = prio ? k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qwl, tb) : 0;
                     if (first_pass && (cc & RS_RES)) {                 // partial: remember its key
                         const int slot = atomicAdd(&sm.npart, 1);
                         if (slot < kMaxPart) {
@@ -415,7 +467,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 }
                 take(key, id, enter);
             };
-            const bool lean = prio && filter_ok && !has_th;    // FP32-bound path (else: exact for all)
             const int64_t gstart = (int64_t)((base + lo) & ~3ull) - (int64_t)base;   // 4-aligned globally
             const int64_t stride = (int64_t)G * 128;
             // cp.async ring: kStages chunks of 128 requests per warp in flight; lane l copies and
@@ -425,7 +476,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
             uint32_t* rst = ring_s + (size_t)warp * kStages * 32;
             auto issue = [&](int64_t g, int slot) {
                 const int64_t e0 = g + 4 * lane;
-                if (g < (int64_t)hi) {
+                if (g + 128 <= (int64_t)hi) {          // full chunk: no bounds arithmetic
+                    cp_async16(ra + slot * 128 + 4 * lane, arr + e0, 16);
+                    cp_async16(ra + slot * 128 + 4 * lane + 2, arr + e0 + 2, 16);
+                    cp_async4(rst + slot * 32 + lane, rsc + e0, 4);
+                } else if (g < (int64_t)hi) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int64_t e = e0 + 2 * h;
@@ -451,6 +506,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 const uint64_t a4[4] = {v0.x, v0.y, v1.x, v1.y};
                 const uint32_t s4 = rst[slot * 32 + lane];
                 const int e0 = (int)(g0 + 4 * lane);
+                if (lean) {
+                    // fast rejection: arrivals after every class's limit, and no partial to record
+                    bool maybe = first_pass && (s4 & 0x08080808u) != 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) maybe |= (int64_t)a4[j] <= amx;
+                    if (!__any_sync(0xFFFFFFFFu, maybe)) continue;
+                }
                 uint32_t qbits = 0;                       // bit j: element j goes to the refine queue
                 bool any_direct = false;
 #pragma unroll
@@ -460,15 +522,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
                     const int c = sb & RS_CLS;
                     if (lean) {
-                        // skip when the exact cap or the FP32 bound proves rank after (kk, ki)
-                        // (a partial always gets its exact key on the first pass: R6 may need it)
+                        // queue when the class's arrival limit cannot rule it out (a partial always
+                        // gets its exact key on the first pass: R6 may need it)
                         const bool part = first_pass && (sb & RS_RES);
-                        bool need = valid && (part || (!((skipm >> c) & 1u) && !(((tiem >> c) & 1u) && (uint32_t)e > ki)));
-                        const uint64_t w = clock - a4[j];
-                        if (need && w != 0 && !((zero_mask >> c) & 1u) && !part) {
-                            const float pf = k1_filter_f32(sm.kp.fS[c], sm.kp.fp2[c], sm.kp.fC2[c], w);
-                            need = !(__fadd_ru(pf, 1e-4f) < thrf);
-                        }
+                        const int64_t am = c == 0 ? am0 : (c == 1 ? am1 : am2);
+                        const bool need = valid && (part || (int64_t)a4[j] <= am);
                         qbits |= need ? (1u << j) : 0u;
                     } else if (!prio) {
                         // exact keys without K1: FCFS / naive aging (key 0, id order, R4) or EDF

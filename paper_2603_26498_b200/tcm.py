@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libtcm.so")
+LIB_PATH = os.environ.get("TCM_LIB_PATH") or os.path.join(_HERE, "_build", "libtcm.so")
 
 TCM_ABI_VERSION = 2
 TCM_OK = 0
