@@ -344,9 +344,12 @@ def _stage_c2(replicas, pending, engine, dev, stream):
 
 
 def time_steps(sim, stream, iters, reps):
-    """Device time of single engine iterations 2..iters+1 (iteration 1 runs request 0 alone)."""
+    """Device time of single engine iterations 2..iters+1 (iteration 1 runs request 0 alone).
+    Returns (kernel ms, call ms, pending): the kernel time is the library's own CUDA-event
+    measurement around its k_step / k_fused launch on its stream (tcm_stats_host.engine_ms);
+    the call time brackets the whole tcm_step call (budget kernel, memsets, active-count read)."""
     import torch
-    times, pend = [], []
+    times, calls, pend = [], [], []
     for rep in range(reps):
         sim.reset()
         sim.step(1)
@@ -360,9 +363,10 @@ def time_steps(sim, stream, iters, reps):
             stream.synchronize()
             s1 = sim.stats()
             if rep > 0:            # first repetition is warm-up
-                times.append(e0.elapsed_time(e1))
+                calls.append(e0.elapsed_time(e1))
+                times.append(s1["engine_ms"] - s0["engine_ms"])
                 pend.append(s1["sum_pending"] - s0["sum_pending"])
-    return float(np.mean(times)), float(np.mean(pend))
+    return float(np.mean(times)), float(np.mean(calls)), float(np.mean(pend))
 
 
 def bench_stepwise(args, dev, stream):
@@ -374,16 +378,16 @@ def bench_stepwise(args, dev, stream):
     out = {}
     for name, R, P in (("C2'", args.step_replicas, args.step_pending), ("C2'-wide", args.step_replicas // 4, args.step_pending * 4)):
         sim = _stage_c2(R, P, tcm.ENGINE_STEPWISE, dev, stream)
-        ms, keys = time_steps(sim, stream, args.step_iters, args.step_reps)
+        ms, call_ms, keys = time_steps(sim, stream, args.step_iters, args.step_reps)
         sim.close()
         fsim = _stage_c2(R, P, tcm.ENGINE_FUSED, dev, stream)
-        fms, _ = time_steps(fsim, stream, args.step_iters, 2)
+        fms, _, _ = time_steps(fsim, stream, args.step_iters, 2)
         fsim.close()
         bytes_per = keys * STEP_BYTES_PER_PENDING + R * STEP_BYTES_PER_DECISION
         achieved = bytes_per / (ms / 1e3) / 1e9
         out[name] = {"kernel": "k_step", "workload": f"{name}: {R} replicas x {P} pending, one iteration (a1-a5)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "ms_per_step": ms, "keys_per_step": keys,
+                     "frac": achieved / peak, "ms_per_step": ms, "call_ms_per_step": call_ms, "keys_per_step": keys,
                      "keys_per_s": keys / (ms / 1e3), "decisions_per_s": R / (ms / 1e3),
                      "fused_engine_ms_per_step": fms}
     prof = os.path.join(ROOT, "profiles", "step_dram_bytes.json")
@@ -396,9 +400,10 @@ def bench_stepwise(args, dev, stream):
     lat = {}
     for eng, nm in ((tcm.ENGINE_STEPWISE, "stepwise"), (tcm.ENGINE_FUSED, "fused")):
         sim = _stage_c2(1, 100_000, eng, dev, stream)
-        ms, keys = time_steps(sim, stream, args.step_iters, args.step_reps)
+        ms, call_ms, keys = time_steps(sim, stream, args.step_iters, args.step_reps)
         sim.close()
         lat[nm + "_us"] = ms * 1e3
+        lat[nm + "_call_us"] = call_ms * 1e3
     lat["pending"] = keys
     out["C2_latency"] = lat
     return out

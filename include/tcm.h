@@ -150,8 +150,8 @@ typedef struct tcm_stats_host {
      * on the context's stream around the library's own launches:                          */
     double reset_ms;           /* the reset: memsets, state init, engine prologue (FUSED: the
                                   class-segment build, row a1)                            */
-    double engine_ms;          /* the step kernels (FUSED: k_fused; STEPWISE: all of its
-                                  per-iteration kernels)                                   */
+    double engine_ms;          /* the step kernels (FUSED: k_fused; STEPWISE: the k_step
+                                  launches, one per engine iteration)                      */
     double stamp_ms;           /* FUSED: k_fstamp (first-token / finish times from the log) */
 } tcm_stats_host;
 

@@ -33,7 +33,7 @@ struct tcm_ctx {
     StepwiseWorkspace sw{};
     uint64_t launches = 0;
     // device timing of the library's launches (tcm_stats_host.*_ms)
-    cudaEvent_t ev[5] = {};              // reset begin/end, engine begin/end, stamp end
+    cudaEvent_t ev[7] = {};              // reset begin/end, engine begin/end, stamp end, k_step begin/end
     bool reset_pending = false;          // ev[0..1] recorded, not yet read
     double reset_ms = 0, engine_ms = 0, stamp_ms = 0;
 };
@@ -216,7 +216,9 @@ tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
         c->launches += 2;
     } else {
         uint64_t l = 0;
-        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, &l);
+        double kms = 0;
+        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, &l, c->ev[5], c->ev[6], &kms);
+        c->engine_ms += kms;
         c->launches += l;
         if (st != TCM_OK) return fail(c, st, "stepwise engine failed: %s", cudaGetErrorString(cudaGetLastError()));
     }
@@ -231,8 +233,10 @@ tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
         c->reset_ms += ms;
         c->reset_pending = false;
     }
-    TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
-    c->engine_ms += ms;
+    if (c->cfg.engine == TCM_ENGINE_FUSED) {
+        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+        c->engine_ms += ms;
+    }
     TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
     c->stamp_ms += ms;
     return TCM_OK;
@@ -256,7 +260,7 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
     if (e == cudaSuccess) e = cudaMalloc(&c->d_active, 4);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_acc, kAccN * 8);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 8);
-    for (int i = 0; i < 5 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    for (int i = 0; i < 7 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     if (e != cudaSuccess) {
         fail(nullptr, TCM_E_CUDA, "tcm_create: %s", cudaGetErrorString(e));
         cudaFree(c->d_active);

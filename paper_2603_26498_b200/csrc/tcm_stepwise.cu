@@ -64,7 +64,9 @@ __device__ __forceinline__ void warp_sort_desc(uint64_t& k, uint32_t& i, int lan
             const uint32_t pi = __shfl_xor_sync(0xFFFFFFFFu, i, j);
             const bool desc = (lane & size) == 0 || size == 32;
             const bool lower = (lane & j) == 0;
-            if ((lower == desc) ? before(pk, pi, k, i) : before(k, i, pk, pi)) {
+            // (key, id) pairs are distinct except the empty (0, NIL), and swapping equal pairs is
+            // harmless, so before(k, i, pk, pi) == !before(pk, pi, k, i) here
+            if (before(pk, pi, k, i) == (lower == desc)) {
                 k = pk;
                 i = pi;
             }
@@ -86,7 +88,7 @@ __device__ __forceinline__ void warp_merge(uint64_t& lk, uint32_t& li, uint64_t 
         const uint64_t pk = __shfl_xor_sync(0xFFFFFFFFu, lk, j);
         const uint32_t pi = __shfl_xor_sync(0xFFFFFFFFu, li, j);
         const bool lower = (lane & j) == 0;
-        if (lower ? before(pk, pi, lk, li) : before(lk, li, pk, pi)) {
+        if (before(pk, pi, lk, li) == lower) {
             lk = pk;
             li = pi;
         }
@@ -557,19 +559,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     }
                 }
                 if (__any_sync(0xFFFFFFFFu, qbits != 0)) {
+                    // append in id order (lane-major, then j) so refined batches follow the
+                    // stream order: exclusive prefix of the per-lane counts from three ballots
+                    const uint32_t nq = __popc(qbits);
+                    const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, nq & 1u);
+                    const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, nq & 2u);
+                    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, nq & 4u);
+                    const uint32_t lt = (1u << lane) - 1u;
+                    int pos = qn + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const bool queue = (qbits >> j) & 1u;
-                        const uint32_t qm = __ballot_sync(0xFFFFFFFFu, queue);
-                        if (queue) {
+                        if ((qbits >> j) & 1u) {
                             const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                            const int pos = qn + __popc(qm & ((1u << lane) - 1));
                             qid[pos] = (uint32_t)(e0 + j);
                             qw[pos] = clock - a4[j];
                             qc[pos] = (uint8_t)((sb & RS_CLS) | (sb & RS_RES));
+                            ++pos;
                         }
-                        qn += __popc(qm);
                     }
+                    qn += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
                     __syncwarp();
                     while (qn >= 32) {
                         refine(32);
@@ -874,7 +882,8 @@ Launch stepwise_config(uint32_t R) {
 }  // namespace
 
 tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWorkspace& w, uint32_t max_iters,
-                        uint32_t* d_active, cudaStream_t s, uint64_t* launches) {
+                        uint32_t* d_active, cudaStream_t s, uint64_t* launches, cudaEvent_t ev_begin,
+                        cudaEvent_t ev_end, double* kernel_ms) {
     uint32_t* remv = reinterpret_cast<uint32_t*>(w.base);
     const Launch L = stepwise_config(t.R);
     k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, max_iters);
@@ -887,6 +896,8 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         uint32_t this_chunk = chunk;
         if ((uint64_t)max_iters - done_launches < this_chunk) this_chunk = (uint32_t)(max_iters - done_launches);
         if (cudaMemsetAsync(d_active, 0, 4, s) != cudaSuccess) return TCM_E_CUDA;
+        // device time of the k_step launches alone (tcm_stats_host.engine_ms)
+        if (cudaEventRecord(ev_begin, s) != cudaSuccess) return TCM_E_CUDA;
         for (uint32_t q = 0; q < this_chunk; ++q) {
             const int last = q + 1 == this_chunk;
             if (L.group == 1) k_step<1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
@@ -894,10 +905,14 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
             (*launches)++;
         }
         done_launches += this_chunk;
+        if (cudaEventRecord(ev_end, s) != cudaSuccess) return TCM_E_CUDA;
         if (cudaGetLastError() != cudaSuccess) return TCM_E_CUDA;
         uint32_t act = 0;
         if (cudaMemcpyAsync(&act, d_active, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TCM_E_CUDA;
         if (cudaStreamSynchronize(s) != cudaSuccess) return TCM_E_CUDA;
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, ev_begin, ev_end) != cudaSuccess) return TCM_E_CUDA;
+        *kernel_ms += ms;
         if (act == 0 || done_launches >= max_iters) break;
     }
     return TCM_OK;
