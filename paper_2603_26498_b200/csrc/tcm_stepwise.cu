@@ -35,7 +35,13 @@ constexpr uint32_t ST_PARTIAL_OVERFLOW = 4;
 constexpr uint8_t RS_CLS = 3, RS_PEND = 4, RS_RES = 8, RS_FT = 16;
 
 // stream staging: per warp, kStages chunks of 128 requests (1 KB arrivals + 128 B states)
-constexpr int kStages = 3;
+#ifndef TCM_SW_STAGES
+#define TCM_SW_STAGES 3
+#endif
+#ifndef TCM_SW_MINB
+#define TCM_SW_MINB 3
+#endif
+constexpr int kStages = TCM_SW_STAGES;
 constexpr size_t kRingBytes = (size_t)kWarpsPerBlock * kStages * (128 * 8 + 32 * 4);
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -261,7 +267,7 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
 }  // namespace
 
 template <int G>
-__global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
+__global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
                                                       int count_active) {
     constexpr int kGroups = kWarpsPerBlock / G;
     constexpr int kMaxDone = GroupSmem<G>::kMaxDone;
@@ -429,7 +435,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                     uint64_t bk = enter ? key : 0;
                     uint32_t bi = enter ? id : NIL;
                     warp_sort_desc(bk, bi, lane);
-                    warp_merge(lk, li, bk, bi, lane);
+                    if (li == NIL && __all_sync(0xFFFFFFFFu, li == NIL)) {   // empty list: the batch is the list
+                        lk = bk;
+                        li = bi;
+                    } else {
+                        warp_merge(lk, li, bk, bi, lane);
+                    }
                     kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
                     ki = __shfl_sync(0xFFFFFFFFu, li, 31);
                 }
@@ -510,9 +521,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_step(ModelConst m, TraceDev t, 
                 const int e0 = (int)(g0 + 4 * lane);
                 if (lean) {
                     // fast rejection: arrivals after every class's limit, and no partial to record
-                    bool maybe = first_pass && (s4 & 0x08080808u) != 0;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) maybe |= (int64_t)a4[j] <= amx;
+                    // (arrivals are sorted, so a lane's first element is its smallest)
+                    const bool maybe = (first_pass && (s4 & 0x08080808u) != 0) || (int64_t)a4[0] <= amx;
                     if (!__any_sync(0xFFFFFFFFu, maybe)) continue;
                 }
                 uint32_t qbits = 0;                       // bit j: element j goes to the refine queue
