@@ -101,6 +101,34 @@ __device__ __forceinline__ void warp_merge(uint64_t& lk, uint32_t& li, uint64_t 
     }
 }
 
+// Compound-key variants for TCM keys (bit patterns of P in [1e-12, 2^17), so key - kKeyBase < 2^58):
+// the tie-break rank rides in the low bits, one 64-bit compare per stage and no id shuffles.
+constexpr uint64_t kKeyBase = 0x3D00000000000000ull;   // bits of 2^-47 < 1e-12
+
+__device__ __forceinline__ void warp_sort_desc_u64(uint64_t& c, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            const uint64_t pc = __shfl_xor_sync(0xFFFFFFFFu, c, j);
+            const bool desc = (lane & size) == 0 || size == 32;
+            const bool lower = (lane & j) == 0;
+            if ((pc > c) == (lower == desc)) c = pc;
+        }
+    }
+}
+
+__device__ __forceinline__ void warp_merge_u64(uint64_t& l, uint64_t b, int lane) {
+    const uint64_t r = __shfl_sync(0xFFFFFFFFu, b, 31 - lane);
+    if (r > l) l = r;
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint64_t p = __shfl_xor_sync(0xFFFFFFFFu, l, j);
+        const bool lower = (lane & j) == 0;
+        if ((p > l) == lower) l = p;
+    }
+}
+
 __device__ __forceinline__ uint64_t warp_incl_scan64(uint64_t v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -332,6 +360,8 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
         }
         group_sync<G>();
         const bool filter_ok = sm.kp.filter_ok != 0;
+        // compound sort keys need every key in [1e-12, 2^17): P <= Smax_c
+        const bool cmp_ok = prio && sm.kp.Smax[0] < 65536.0 && sm.kp.Smax[1] < 65536.0 && sm.kp.Smax[2] < 65536.0;
         const uint32_t zero_mask = sm.kp.zero_mask;
 
         for (int pass = 0;; ++pass) {
@@ -431,11 +461,35 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                         kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
                         ki = __shfl_sync(0xFFFFFFFFu, li, 31);
                     }
+                } else if (cmp_ok) {
+                    // TCM keys: compound sort.  Batch lanes are in id order (the refine queue is
+                    // id-ordered), and every list entry precedes every batch entry in id, so the
+                    // rank bits (31 - lane; list above batch) encode the (key desc, id asc) tie-break.
+                    uint64_t c = enter ? (((key - kKeyBase) << 5) | (uint64_t)(31 - lane)) : 0;
+                    warp_sort_desc_u64(c, lane);
+                    const uint32_t sid = __shfl_sync(0xFFFFFFFFu, id, 31 - (int)(c & 31));
+                    const uint64_t bk = c ? (c >> 5) + kKeyBase : 0;
+                    const uint32_t bi = c ? sid : NIL;
+                    if (__all_sync(0xFFFFFFFFu, li == NIL)) {
+                        lk = bk;
+                        li = bi;
+                    } else {
+                        uint64_t lc = li != NIL ? (((lk - kKeyBase) << 6) | 32u | (uint64_t)(31 - lane)) : 0;
+                        const uint64_t bc = bi != NIL ? (((bk - kKeyBase) << 6) | (uint64_t)(31 - lane)) : 0;
+                        warp_merge_u64(lc, bc, lane);
+                        const int pos = 31 - (int)(lc & 31);
+                        const uint32_t fl = __shfl_sync(0xFFFFFFFFu, li, pos);
+                        const uint32_t fb = __shfl_sync(0xFFFFFFFFu, bi, pos);
+                        li = lc == 0 ? NIL : ((lc & 32) ? fl : fb);
+                        lk = lc == 0 ? 0 : (lc >> 6) + kKeyBase;
+                    }
+                    kk = __shfl_sync(0xFFFFFFFFu, lk, 31);
+                    ki = __shfl_sync(0xFFFFFFFFu, li, 31);
                 } else {
                     uint64_t bk = enter ? key : 0;
                     uint32_t bi = enter ? id : NIL;
                     warp_sort_desc(bk, bi, lane);
-                    if (li == NIL && __all_sync(0xFFFFFFFFu, li == NIL)) {   // empty list: the batch is the list
+                    if (__all_sync(0xFFFFFFFFu, li == NIL)) {   // empty list: the batch is the list
                         lk = bk;
                         li = bi;
                     } else {
