@@ -6,6 +6,7 @@ no code with it.  The arithmetic lives in tcm_oracle.c (plain C, gcc -O2
 -ffp-contract=off); this file only marshals numpy arrays through ctypes.
 
 Parity status: every function is pinned by tests/test_oracle_*.py
+(simulate_growth, the NEXT-1 loop, by tests/test_oracle_next1.py)
 except full random traces, whose schedules have no independent closed form ("parity
 unpinned" beyond the invariants, reductions, hand-worked schedules and brute force).
 """
@@ -103,6 +104,9 @@ def lib():
         L.orc_simulate.restype = i
         L.orc_simulate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32] + \
             [ctypes.c_void_p] * 10 + [ctypes.c_void_p, u64, ctypes.c_void_p, u64]
+        L.orc_simulate_growth.restype = i
+        L.orc_simulate_growth.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32] + \
+            [ctypes.c_void_p] * 14 + [u64]
         L.orc_ttft_bucket.restype = ctypes.c_uint32
         L.orc_ttft_bucket.argtypes = [u64]
         L.orc_aggregate.restype = None
@@ -219,6 +223,57 @@ def simulate(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM,
         assert log_n.value <= cap, "iteration log overflow"
         iters = logbuf[: log_n.value].copy()
     return Result(seq, ft, dn, cl, counters, iters, st)
+
+
+@dataclass
+class GrowthResult:
+    admit_seq: np.ndarray
+    first_token_us: np.ndarray
+    done_us: np.ndarray
+    preempt_count: np.ndarray
+    preempted_us: np.ndarray
+    cls: np.ndarray
+    counters: dict
+    status: int
+
+
+def simulate_growth(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM, alpha=1.0,
+                    kv_capacity=131072, chunk_budget=2048, m: OrcModel | None = None,
+                    max_iters: int = 0, admit_skip: bool = False) -> GrowthResult:
+    """NEXT-1 engine loop: decode KV growth + preemption by recomputation (R28-R32)."""
+    m = m or model()
+    a = np.ascontiguousarray(arrival_us, dtype=np.uint64)
+    f = np.ascontiguousarray(footprint, dtype=np.uint32)
+    il = np.ascontiguousarray(inline_us, dtype=np.uint32)
+    o = np.ascontiguousarray(out_tokens, dtype=np.uint16)
+    md = np.ascontiguousarray(modality, dtype=np.uint8)
+    n = len(a)
+    seq = np.full(n, 0xFFFFFFFF, np.uint32)
+    ft = np.zeros(n, np.uint64)
+    dn = np.zeros(n, np.uint64)
+    pc = np.zeros(n, np.uint32)
+    pt = np.zeros(n, np.uint64)
+    cl = np.zeros(n, np.uint8)
+    cnt = OrcCounters()
+    npre, nforced = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    r = OrcReplica(policy, chunk_budget, kv_capacity, alpha, int(admit_skip), 0)
+    st = lib().orc_simulate_growth(
+        ctypes.byref(m), ctypes.byref(r), n, a.ctypes.data, f.ctypes.data, il.ctypes.data,
+        o.ctypes.data, md.ctypes.data, seq.ctypes.data, ft.ctypes.data, dn.ctypes.data,
+        pc.ctypes.data, pt.ctypes.data, cl.ctypes.data, ctypes.byref(cnt), ctypes.byref(npre),
+        ctypes.byref(nforced), max_iters)
+    counters = {name: getattr(cnt, name) for name, _ in OrcCounters._fields_}
+    counters["preemptions"] = npre.value
+    counters["forced_preemptions"] = nforced.value
+    return GrowthResult(seq, ft, dn, pc, pt, cl, counters, st)
+
+
+def simulate_trace_growth(tr, r: int, policy=TCM, alpha=1.0, kv_capacity=131072, chunk_budget=2048,
+                          m=None, max_iters=0, admit_skip=False) -> GrowthResult:
+    a, b = int(tr.offset[r]), int(tr.offset[r + 1])
+    return simulate_growth(tr.arrival_us[a:b], tr.footprint[a:b], tr.inline_us[a:b],
+                           tr.out_tokens[a:b], tr.modality[a:b], policy, alpha, kv_capacity,
+                           chunk_budget, m, max_iters, admit_skip)
 
 
 def simulate_trace(tr, r: int, policy=TCM, alpha=1.0, kv_capacity=131072, chunk_budget=2048,

@@ -347,6 +347,211 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
 }
 
 /* ------------------------------------------------------------------------------ */
+/* NEXT-1: decode KV growth + preemption by recomputation (R28-R32).  */
+/* Written as its own loop (the R7 loop above stays as pinned); request phases are  */
+/* kept per id and every set is a plain scan over ids 0..nxt-1, in id order.        */
+/* ------------------------------------------------------------------------------ */
+enum { PH_WAIT = 1, PH_PREFILL = 2, PH_DECODE = 3, PH_DONE = 4 };
+
+int orc_simulate_growth(const orc_model* m, const orc_replica* r, uint32_t n,
+                        const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
+                        const uint16_t* out, const uint8_t* mod, uint32_t* admit_seq,
+                        uint64_t* first_token, uint64_t* done, uint32_t* pcount,
+                        uint64_t* ptime, uint8_t* cls_out, orc_counters* cnt,
+                        uint64_t* n_preempt, uint64_t* n_forced, uint64_t max_iters)
+{
+    memset(cnt, 0, sizeof(*cnt));
+    *n_preempt = 0;
+    *n_forced = 0;
+    if (r->chunk_budget == 0 || r->policy > ORC_NAIVE_AGING || r->admit_skip > 1) return -1;
+    for (uint32_t i = 0; i < n; ++i) {
+        /* R28: the largest allocation a request can reach must fit on its own */
+        if (f[i] == 0 || out[i] == 0 || mod[i] > 2) return -1;
+        if ((uint64_t)f[i] + out[i] - 1 > r->kv_capacity) return -1;
+        if (i > 0 && arrival[i] < arrival[i - 1]) return -1;
+    }
+    double C[3];
+    int zero[3];
+    for (int c = 0; c < 3; ++c) C[c] = orc_k1_const(r->alpha, m->k[c], m->p[c], &zero[c]);
+
+    uint8_t* ph = (uint8_t*)calloc(n + 1, 1);
+    uint8_t* admitted = (uint8_t*)calloc(n + 1, 1);
+    uint8_t* emitted = (uint8_t*)calloc(n + 1, 1);     /* first token emitted */
+    uint32_t* rem = (uint32_t*)calloc(n + 1, 4);
+    uint32_t* held = (uint32_t*)calloc(n + 1, 4);
+    uint32_t* gen = (uint32_t*)calloc(n + 1, 4);
+    uint64_t* pstart = (uint64_t*)calloc(n + 1, 8);
+    orc_entry* order = (orc_entry*)malloc(sizeof(orc_entry) * (n + 1));
+    if (!ph || !admitted || !emitted || !rem || !held || !gen || !pstart || !order) {
+        free(ph); free(admitted); free(emitted); free(rem); free(held); free(gen); free(pstart); free(order);
+        return -1;
+    }
+    for (uint32_t i = 0; i < n; ++i) { pcount[i] = 0; ptime[i] = 0; }
+
+    uint64_t clock = 0, kv_free = r->kv_capacity, iter = 0;
+    uint32_t nxt = 0, seq = 0;
+    int status = 0;
+    for (;;) {
+        if (max_iters && iter >= max_iters) break;
+        /* 1 ingest */
+        while (nxt < n && arrival[nxt] <= clock) {
+            cls_out[nxt] = (uint8_t)orc_classify(m, mod[nxt], f[nxt]);
+            ph[nxt] = PH_WAIT;
+            rem[nxt] = f[nxt];
+            ++nxt;
+        }
+        uint32_t n_pend = 0, n_dec = 0;
+        for (uint32_t i = 0; i < nxt; ++i) {
+            if (ph[i] == PH_WAIT || ph[i] == PH_PREFILL) n_pend++;
+            if (ph[i] == PH_DECODE) n_dec++;
+        }
+        /* 2 idle jump (R15) */
+        if (n_pend == 0 && n_dec == 0) {
+            if (nxt == n) break;
+            clock = arrival[nxt];
+            cnt->idle_jumps++;
+            continue;
+        }
+        /* 3a memory exhaustion: one KV token per decoding sequence this iteration (R28);
+         * preempt victims until it fits (R29) */
+        while (kv_free < n_dec) {
+            uint32_t v = UINT32_MAX;
+            int forced = 0;
+            if (r->policy == ORC_TCM) {
+                /* the running request ranked last by (P desc, arrival asc, id asc),
+                 * motorcycles only when no other class is running */
+                for (int pass = 0; pass < 2 && v == UINT32_MAX; ++pass) {
+                    double vP = 0.0;
+                    for (uint32_t i = 0; i < nxt; ++i) {
+                        if (ph[i] != PH_PREFILL && ph[i] != PH_DECODE) continue;
+                        int c = cls_out[i];
+                        if (pass == 0 && c == 0) continue;
+                        double P = orc_priority(m->S[c], m->p[c], C[c], zero[c], clock - arrival[i]);
+                        uint64_t kb = orc_key_bits(P), vb = orc_key_bits(vP);
+                        /* later in the order: smaller key, or equal key and later (arrival, id) */
+                        if (v == UINT32_MAX || kb < vb || (kb == vb && i > v)) { v = i; vP = P; }
+                    }
+                    forced = pass == 1;
+                }
+            } else {
+                for (uint32_t i = 0; i < nxt; ++i)       /* most recently arrived */
+                    if (ph[i] == PH_PREFILL || ph[i] == PH_DECODE) v = i;
+            }
+            if (v == UINT32_MAX) { status = -2; break; }   /* unreachable: n_dec > 0 */
+            if (ph[v] == PH_DECODE) { n_dec--; n_pend++; }
+            kv_free += held[v];
+            rem[v] = held[v];          /* recomputation: prompt + generated tokens again (R30) */
+            held[v] = 0;
+            ph[v] = PH_WAIT;
+            pcount[v]++;
+            pstart[v] = clock;
+            (*n_preempt)++;
+            if (forced) (*n_forced)++;
+        }
+        if (status) break;
+        /* 3b the decode tokens of this iteration take their KV */
+        kv_free -= n_dec;
+        for (uint32_t i = 0; i < nxt; ++i)
+            if (ph[i] == PH_DECODE) held[i]++;
+        uint32_t Bp = r->chunk_budget > n_dec ? r->chunk_budget - n_dec : 0;
+
+        /* 4-5 order the pending requests (as orc_simulate) */
+        uint32_t np = 0;
+        for (uint32_t i = 0; i < nxt; ++i) {
+            if (ph[i] != PH_WAIT && ph[i] != PH_PREFILL) continue;
+            order[np].id = i;
+            order[np].arrival = arrival[i];
+            order[np].P = 0.0;
+            order[np].dl = 0;
+            if (r->policy == ORC_TCM) {
+                int c = cls_out[i];
+                order[np].P = orc_priority(m->S[c], m->p[c], C[c], zero[c], clock - arrival[i]);
+            } else if (r->policy == ORC_EDF) {
+                order[np].dl = arrival[i] * m->slo_den +
+                               m->slo_num * orc_iso_e2e(m, r->chunk_budget, f[i], inl[i], out[i]);
+            } else if (r->policy == ORC_NAIVE_AGING) {
+                order[np].dl = clock - arrival[i];
+            }
+            np++;
+        }
+        if (r->policy == ORC_TCM) qsort(order, np, sizeof(orc_entry), orc_cmp);
+        if (r->policy == ORC_EDF) qsort(order, np, sizeof(orc_entry), orc_cmp_edf);
+        if (r->policy == ORC_NAIVE_AGING) qsort(order, np, sizeof(orc_entry), orc_cmp_age);
+
+        /* 6 admission scan (R5-R8); a re-admission reserves what it will re-prefill (R30) */
+        uint32_t left = Bp;
+        int blocked = 0;
+        uint64_t tok = 0, inl_sum = 0;
+        for (uint32_t q = 0; q < np; ++q) {
+            uint32_t i = order[q].id;
+            if (left == 0) break;
+            if (ph[i] == PH_WAIT) {
+                if (blocked) continue;
+                if ((uint64_t)rem[i] > kv_free) { blocked = !r->admit_skip; continue; }
+                ph[i] = PH_PREFILL;
+                held[i] = rem[i];
+                kv_free -= rem[i];
+                if (!admitted[i]) {
+                    admitted[i] = 1;
+                    admit_seq[i] = seq++;
+                    inl_sum += inl[i];
+                } else {
+                    ptime[i] += clock - pstart[i];       /* R31 */
+                }
+            }
+            uint32_t c = rem[i] < left ? rem[i] : left;
+            rem[i] -= c;
+            left -= c;
+            tok += c;
+        }
+        if (tok == 0 && n_dec == 0) { status = -2; break; }
+
+        /* 8 cost and clock */
+        clock += m->c0_us + m->cp_us * tok + m->cd_us * (uint64_t)n_dec + inl_sum;
+        iter++;
+        cnt->iterations++;
+        if (np > 0) {
+            cnt->decisions++;
+            cnt->sum_pending += np;
+            if (np > cnt->max_pending) cnt->max_pending = np;
+        }
+        /* 9 decode tokens; finished sequences release everything they hold */
+        for (uint32_t i = 0; i < nxt; ++i) {
+            if (ph[i] != PH_DECODE) continue;
+            gen[i]++;
+            if (gen[i] == out[i]) {
+                done[i] = clock;
+                kv_free += held[i];
+                held[i] = 0;
+                ph[i] = PH_DONE;
+            }
+        }
+        /* 10 completed prefills emit a token: the first one (R12) or, after a re-prefill,
+         * the next one (R30) */
+        for (uint32_t i = 0; i < nxt; ++i) {
+            if (ph[i] != PH_PREFILL || rem[i] != 0) continue;
+            if (!emitted[i]) {
+                emitted[i] = 1;
+                first_token[i] = clock;
+            }
+            gen[i]++;
+            if (gen[i] == out[i]) {
+                done[i] = clock;
+                kv_free += held[i];
+                held[i] = 0;
+                ph[i] = PH_DONE;
+            } else {
+                ph[i] = PH_DECODE;
+            }
+        }
+    }
+    cnt->admitted = seq;
+    cnt->final_clock = clock;
+    free(ph); free(admitted); free(emitted); free(rem); free(held); free(gen); free(pstart); free(order);
+    return status;
+}
+
+/* ------------------------------------------------------------------------------ */
 /* a6: result aggregation (PAPER.md:579 SLO = 5x isolated E2E).   */
 /* ------------------------------------------------------------------------------ */
 

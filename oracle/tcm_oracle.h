@@ -108,6 +108,29 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
                  orc_iter_rec* iter_log, uint64_t log_cap, uint64_t* log_n,
                  uint64_t max_iters);
 
+/*
+ * NEXT-1: the same engine loop with decode KV growth and preemption by
+ * recomputation, readings R28-R32.  A running request holds its reservation plus
+ * one KV token per decode iteration run.  At the start of every iteration, while
+ * the free KV cannot cover one token per decoding sequence, a victim among the running requests
+ * (reserved partial prefills and decoding sequences) is preempted (SPEC.md:87, 398, 402, 455(3)):
+ * FCFS (and every non-TCM policy) takes the most recently arrived; TCM the lowest-ranked
+ * non-motorcycle, a motorcycle only when every running request is one (counted in *n_forced).
+ * The victim frees everything it holds and waits again with its original arrival;
+ * its next admission reserves and re-prefills what it held, charges no inline time and takes
+ * no admit_seq; completing that re-prefill emits its next token.  Per request also:
+ * preempt_count and preempted_us (from the preemption to the next admission).
+ * Requires footprint + out - 1 <= kv_capacity for every request (else -1).
+ */
+int orc_simulate_growth(const orc_model* m, const orc_replica* r, uint32_t n,
+                        const uint64_t* arrival_us, const uint32_t* footprint,
+                        const uint32_t* inline_us, const uint16_t* out_tokens,
+                        const uint8_t* modality,
+                        uint32_t* admit_seq, uint64_t* first_token_us, uint64_t* done_us,
+                        uint32_t* preempt_count, uint64_t* preempted_us,
+                        uint8_t* cls_out, orc_counters* cnt,
+                        uint64_t* n_preempt, uint64_t* n_forced, uint64_t max_iters);
+
 /* ---- a6 aggregation: HDR-style TTFT bucket and per-group counters ---- */
 enum { ORC_HIST_BINS = 496, ORC_GROUPS = 4, ORC_NCNT = 6 };
 uint32_t orc_ttft_bucket(uint64_t ttft_us);

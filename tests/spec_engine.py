@@ -32,12 +32,13 @@ def iso_e2e(f, inl, out, B, c0=5000, cp=20, cd=500):
 
 
 def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
-        thr=((4096, 2**32 - 1), (0, 2**32 - 1), (0, 8192)), skip=False, slo=5):
+        thr=((4096, 2**32 - 1), (0, 2**32 - 1), (0, 8192)), skip=False, slo=5, growth=False):
     """reqs: list of (arrival_us, footprint, inline_us, out, modality); policy: 0 FCFS, 1 TCM,
-    2 EDF (deadline = arrival + slo x isolated E2E), 3 naive aging.  Returns dict of lists."""
+    2 EDF (deadline = arrival + slo x isolated E2E), 3 naive aging.  growth=True: NEXT-1 decode
+    KV growth and preemption by recomputation (R28-R32).  Returns dict of lists."""
     n = len(reqs)
     R = [dict(id=i, arr=a, f=f, inl=il, out=o, cls=classify(m, f, thr), state="future",
-              rem=f, gen=0, admit=None, first=None, done=None)
+              rem=f, gen=0, admit=None, first=None, done=None, held=0, npre=0, tpre=0, since=None)
          for i, (a, f, il, o, m) in enumerate(reqs)]
     clock, free, seq = 0, kv, 0
     near_tie = False
@@ -53,6 +54,31 @@ def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
                 break
             clock = min(fut)
             continue
+        if growth:
+            # R28/R29: the decode tokens of this iteration need len(dec) free KV tokens; the
+            # victim is the running request that comes LAST in the policy's order (TCM: by
+            # priority among non-motorcycles first; otherwise: latest arrival)
+            while free < len(dec):
+                running = [r for r in R if r["state"] in ("partial", "decoding")]
+                if policy == 1:
+                    pool = [r for r in running if r["cls"] != 0] or running
+                    keyed = sorted(((max(paper_priority(r["cls"], clock - r["arr"], alpha), 1e-12), r)
+                                    for r in pool), key=lambda t: (-t[0], t[1]["arr"], t[1]["id"]))
+                    if len(keyed) > 1 and keyed[-2][1]["cls"] != keyed[-1][1]["cls"] and \
+                            abs(keyed[-2][0] - keyed[-1][0]) < 1e-11:
+                        near_tie = True
+                    v = keyed[-1][1]
+                else:
+                    v = max(running, key=lambda r: (r["arr"], r["id"]))
+                free += v["held"]
+                v["rem"], v["held"] = v["held"], 0          # R30: recompute what it held
+                v["state"], v["since"] = "waiting", clock
+                v["npre"] += 1
+                dec = [r for r in R if r["state"] == "decoding"]
+            pend = [r for r in R if r["state"] in ("waiting", "partial")]
+            free -= len(dec)
+            for r in dec:
+                r["held"] += 1
         budget = max(0, B - len(dec))                     # step 3 (R8)
         if policy == 1:                                   # steps 4-5 (R2-R5)
             keyed = [(max(paper_priority(r["cls"], clock - r["arr"], alpha), 1e-12), r) for r in pend]
@@ -73,16 +99,21 @@ def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
             if left == 0:
                 break
             if r["state"] == "waiting":
+                need = r["rem"] if growth else r["f"]
                 if blocked:
                     continue
-                if r["f"] > free:
+                if need > free:
                     blocked = not skip
                     continue
                 r["state"] = "partial"
-                free -= r["f"]
-                r["admit"] = seq
-                seq += 1
-                inl += r["inl"]
+                free -= need
+                r["held"] = need
+                if r["admit"] is None:
+                    r["admit"] = seq
+                    seq += 1
+                    inl += r["inl"]
+                else:                                     # R31: back from preemption
+                    r["tpre"] += clock - r["since"]
             chunk = min(r["rem"], left)
             r["rem"] -= chunk
             left -= chunk
@@ -93,14 +124,17 @@ def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
             r["gen"] += 1
             if r["gen"] == r["out"]:
                 r["state"], r["done"] = "finished", clock
-                free += r["f"]
-        for r in pend:                                    # step 10 (R12)
+                free += r["held"] if growth else r["f"]
+        for r in pend:                                    # step 10 (R12; R30 after a re-prefill)
             if r["state"] == "partial" and r["rem"] == 0:
-                r["first"], r["gen"] = clock, 1
-                if r["out"] == 1:
+                if r["first"] is None:
+                    r["first"] = clock
+                r["gen"] += 1
+                if r["gen"] == r["out"]:
                     r["state"], r["done"] = "finished", clock
-                    free += r["f"]
+                    free += r["held"] if growth else r["f"]
                 else:
                     r["state"] = "decoding"
     return dict(admit_seq=[r["admit"] for r in R], first=[r["first"] for r in R],
-                done=[r["done"] for r in R], near_tie=near_tie)
+                done=[r["done"] for r in R], preempt_count=[r["npre"] for r in R],
+                preempted_us=[r["tpre"] for r in R], near_tie=near_tie)
