@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define TCM_ABI_VERSION 2u
+#define TCM_ABI_VERSION 3u
 
 typedef int32_t tcm_status;
 #define TCM_OK 0
@@ -65,6 +65,14 @@ enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1, TCM_POLICY_EDF = 2, TCM_POLICY_N
 /* tcm_replica_params.flags */
 #define TCM_ADMIT_SKIP 1u   /* a KV misfit is skipped instead of stopping new admissions (first
                                fit; the alternative reading of R6, NEXT-3).  STEPWISE only. */
+#define TCM_KV_GROWTH 2u    /* NEXT-1: decode KV growth + preemption by recomputation (readings
+                               R28-R32).  A running
+                               request holds its reservation plus one KV token per decode
+                               iteration; when the free KV cannot cover this iteration's decode
+                               tokens, victims are preempted (FCFS/EDF/naive aging: most recently
+                               arrived; TCM: lowest-ranked non-motorcycle) and re-prefill what
+                               they held.  Needs footprint + out - 1 <= kv_capacity for every
+                               request (else TCM_E_CAPACITY).  STEPWISE only.                */
 
 enum { TCM_ENGINE_FUSED = 0, TCM_ENGINE_STEPWISE = 1 };
 /* FUSED   : one persistent thread per replica runs the whole step loop in registers;
@@ -128,6 +136,9 @@ typedef struct tcm_results_view {
     uint32_t* admit_seq;          /* [N] order of first admission within the replica    */
     uint64_t* first_token_us;     /* [N] clock at the first token (TTFT = - arrival)    */
     uint64_t* done_us;            /* [N] clock at completion                            */
+    uint32_t* preempt_count;      /* [N] preemptions of the request (TCM_KV_GROWTH; else 0) */
+    uint64_t* preempted_us;       /* [N] time from each preemption to the next admission,
+                                     summed                                 */
 } tcm_results_view;
 
 /* Work counters (sums over all replicas of this context). */
@@ -153,6 +164,8 @@ typedef struct tcm_stats_host {
     double engine_ms;          /* the step kernels (FUSED: k_fused; STEPWISE: the k_step
                                   launches, one per engine iteration)                      */
     double stamp_ms;           /* FUSED: k_fstamp (first-token / finish times from the log) */
+    uint64_t preemptions;      /* TCM_KV_GROWTH: preemptions (R29)                     */
+    uint64_t forced_preemptions; /* TCM: motorcycle victims (only when nothing else ran)  */
 } tcm_stats_host;
 
 typedef struct tcm_ctx tcm_ctx;

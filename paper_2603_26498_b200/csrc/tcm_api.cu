@@ -29,7 +29,7 @@ struct tcm_ctx {
     tcm_results_view host_res{};
     uint32_t* d_active = nullptr;        // [1]
     unsigned long long* d_acc = nullptr; // [kAccN]
-    uint32_t* d_val = nullptr;           // [2]
+    uint32_t* d_val = nullptr;           // [3] worst status, first bad replica, any TCM_KV_GROWTH
     StepwiseWorkspace sw{};
     uint64_t launches = 0;
     // device timing of the library's launches (tcm_stats_host.*_ms)
@@ -148,6 +148,7 @@ size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) 
     b += (size_t)R * sizeof(ClassPack);
     b += 20 * N;                                 // results kept on device when not supplied
     if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += stepwise_workspace_bytes(R, N) + 8 * N;
+    if (cfg && cfg->engine == TCM_ENGINE_STEPWISE) b += 40 * N;   // NEXT-1 per-request state + results
     if (host_mirror) b += (size_t)(R + 1) * 8 + 19 * N + (size_t)R * sizeof(tcm_replica_params);
     return b;
 }
@@ -161,6 +162,10 @@ tcm_status copy_results_to_host(tcm_ctx* c) {
         TCM_CUDA(c, cudaMemcpyAsync(c->host_res.first_token_us, c->t.first_token, 8 * N, cudaMemcpyDeviceToHost, c->s));
     if (c->host_res.done_us)
         TCM_CUDA(c, cudaMemcpyAsync(c->host_res.done_us, c->t.done, 8 * N, cudaMemcpyDeviceToHost, c->s));
+    if (c->host_res.preempt_count && c->t.pcount)
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.preempt_count, c->t.pcount, 4 * N, cudaMemcpyDeviceToHost, c->s));
+    if (c->host_res.preempted_us && c->t.ptime)
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.preempted_us, c->t.ptime, 8 * N, cudaMemcpyDeviceToHost, c->s));
     return TCM_OK;
 }
 
@@ -191,6 +196,9 @@ tcm_status reset_state(tcm_ctx* c) {
     TCM_CUDA(c, cudaMemsetAsync(t.done, 0, 8 * N, s));
     TCM_CUDA(c, cudaMemsetAsync(t.admit_seq, 0xFF, 4 * N, s));
     if (t.req_state) TCM_CUDA(c, cudaMemsetAsync(t.req_state, 0, N ? N : 1, s));
+    if (t.pcount) TCM_CUDA(c, cudaMemsetAsync(t.pcount, 0, 4 * (N ? N : 1), s));
+    if (t.ptime) TCM_CUDA(c, cudaMemsetAsync(t.ptime, 0, 8 * (N ? N : 1), s));
+    if (t.genp) TCM_CUDA(c, cudaMemsetAsync(t.genp, 0, 4 * (N ? N : 1), s));
     launch_init(t, s);
     c->launches++;
     if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
@@ -259,7 +267,7 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
     cudaError_t e = cudaGetDevice(&c->device);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_active, 4);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_acc, kAccN * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 8);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 12);
     for (int i = 0; i < 7 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     if (e != cudaSuccess) {
         fail(nullptr, TCM_E_CUDA, "tcm_create: %s", cudaGetErrorString(e));
@@ -372,23 +380,41 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         c->sw = stepwise_bind(p, R);
         if ((st = dalloc(c, &p, 8 * (N ? N : 1)))) return st;
         t.deadline = (uint64_t*)p;
+        // NEXT-1 (TCM_KV_GROWTH) per-request state and results
+        const uint64_t Nn = N ? N : 1;
+        if ((st = dalloc(c, &p, 4 * Nn))) return st;
+        t.kvres = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 4 * Nn))) return st;
+        t.kvfin = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 8 * Nn))) return st;
+        t.fin = (uint64_t*)p;
+        if ((st = dalloc(c, &p, 4 * Nn))) return st;
+        t.genp = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 8 * Nn))) return st;
+        t.pstart = (uint64_t*)p;
+        if (dev_res && rv->preempt_count) t.pcount = rv->preempt_count;
+        else { if ((st = dalloc(c, &p, 4 * Nn))) return st; t.pcount = (uint32_t*)p; }
+        if (dev_res && rv->preempted_us) t.ptime = rv->preempted_us;
+        else { if ((st = dalloc(c, &p, 8 * Nn))) return st; t.ptime = (uint64_t*)p; }
     }
 
     c->t = t;
 
     // validate on the device (R18) before any kernel reads the trace
-    uint32_t hv[2] = {0, 0xFFFFFFFFu};
-    TCM_CUDA(c, cudaMemcpyAsync(c->d_val, hv, 8, cudaMemcpyHostToDevice, s));
+    uint32_t hv[3] = {0, 0xFFFFFFFFu, 0};
+    TCM_CUDA(c, cudaMemcpyAsync(c->d_val, hv, 12, cudaMemcpyHostToDevice, s));
     launch_validate(t, c->d_val, c->cfg.engine == TCM_ENGINE_STEPWISE, s);
     c->launches++;
     TCM_CUDA(c, cudaGetLastError());
-    TCM_CUDA(c, cudaMemcpyAsync(hv, c->d_val, 8, cudaMemcpyDeviceToHost, s));
+    TCM_CUDA(c, cudaMemcpyAsync(hv, c->d_val, 12, cudaMemcpyDeviceToHost, s));
     TCM_CUDA(c, cudaStreamSynchronize(s));
+    c->t.any_growth = hv[2];
+    t.any_growth = hv[2];
     if (hv[0] == ST_CAPACITY)
-        return fail(c, TCM_E_CAPACITY, "replica %u: a footprint exceeds kv_capacity (R18)", hv[1]);
+        return fail(c, TCM_E_CAPACITY, "replica %u: a footprint (with TCM_KV_GROWTH: footprint + out - 1) exceeds kv_capacity (R18, R28)", hv[1]);
     if (hv[0] != ST_OK)
         return fail(c, TCM_E_ARG, "replica %u: malformed trace or params (footprint/out/modality/"
-                    "arrival order/policy/budget/kv/alpha/flags; EDF, TCM_ADMIT_SKIP and replicas of "
+                    "arrival order/policy/budget/kv/alpha/flags; EDF, TCM_ADMIT_SKIP, TCM_KV_GROWTH and replicas of "
                     ">= 2^24 requests need the "
                     "stepwise engine)", hv[1]);
     launch_kpack(c->m, t, s);                 // params are validated: K1 class constants once
@@ -459,6 +485,8 @@ tcm_status tcm_stats(tcm_ctx* c, tcm_stats_host* out, int64_t* dev_hist, int64_t
         out->replicas_done = h[kAccReplicasDone];
         out->replicas_active = h[kAccReplicasActive];
         out->scanned_decisions = h[kAccScanned];
+        out->preemptions = h[kAccPreempt];
+        out->forced_preemptions = h[kAccForced];
         out->first_bad_replica = h[kAccBadStatus] ? (int32_t)h[kAccBadReplica] : -1;
         out->first_bad_status = (int32_t)h[kAccBadStatus];
         if (c->reset_pending) {

@@ -77,10 +77,11 @@ __global__ void k_validate(TraceDev t, uint32_t* v, int general_ok) {
     uint32_t bad = ST_OK;
     if (b < a || b > t.N || b - a >= 0xFFFFFFFFull) bad = ST_BAD_INPUT;
     if (p.policy > TCM_POLICY_NAIVE_AGING || p.chunk_budget == 0 || p.kv_capacity == 0 ||
-        p.kv_capacity > 0xFFFFFFFFull || !(p.aging_alpha >= 0.0) || (p.flags & ~TCM_ADMIT_SKIP) != 0)
+        p.kv_capacity > 0xFFFFFFFFull || !(p.aging_alpha >= 0.0) || (p.flags & ~(TCM_ADMIT_SKIP | TCM_KV_GROWTH)) != 0)
         bad = ST_BAD_INPUT;
     // EDF and first-fit admission break Lemmas L1/L2: only the stepwise engine runs them
-    if (!general_ok && (p.policy == TCM_POLICY_EDF || (p.flags & TCM_ADMIT_SKIP))) bad = ST_BAD_INPUT;
+    if (!general_ok && (p.policy == TCM_POLICY_EDF || (p.flags & (TCM_ADMIT_SKIP | TCM_KV_GROWTH)))) bad = ST_BAD_INPUT;
+    const bool growth = (p.flags & TCM_KV_GROWTH) != 0;
     // fused calendar slots count finishing requests in 24 bits
     if (!general_ok && b - a >= (1ull << (64 - kCalCntShift))) bad = ST_BAD_INPUT;
     if (bad == ST_OK) {
@@ -90,9 +91,11 @@ __global__ void k_validate(TraceDev t, uint32_t* v, int general_ok) {
             if (f == 0 || o == 0 || o > kCalSlots || t.mod[i] > 2) bad = bad > ST_BAD_INPUT ? bad : ST_BAD_INPUT;
             if (i > a && t.arrival[i] < t.arrival[i - 1]) bad = bad > ST_BAD_INPUT ? bad : ST_BAD_INPUT;
             if ((uint64_t)f > p.kv_capacity) bad = ST_CAPACITY;
+            if (growth && o >= 1 && (uint64_t)f + o - 1 > p.kv_capacity) bad = ST_CAPACITY;   // R28
         }
     }
     // ST_BAD_INPUT (2) vs ST_CAPACITY (3): report the larger code
+    if (lane == 0 && growth) atomicOr(&v[2], 1u);
     const uint32_t worst = __reduce_max_sync(0xFFFFFFFFu, bad);
     if (lane == 0 && worst != ST_OK) {
         atomicMax(&v[0], worst);
@@ -112,7 +115,7 @@ __global__ void k_reduce(TraceDev t, unsigned long long* acc /* [kAccN] */) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     ReplicaState st;
     bool live = r < t.R;
-    uint64_t v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint64_t v[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t mx = 0;
     if (live) {
         st = t.state[r];
@@ -125,6 +128,8 @@ __global__ void k_reduce(TraceDev t, unsigned long long* acc /* [kAccN] */) {
         v[6] = (st.flags & FLAG_FINISHED) ? 1 : 0;
         v[7] = (st.flags & FLAG_FINISHED) ? 0 : 1;
         v[8] = st.scanned;
+        v[9] = st.tail[1];       // stepwise: preemptions (NEXT-1)
+        v[10] = st.tail[2];      // stepwise: forced (motorcycle) preemptions
         mx = st.max_pending;
         if (st.status != ST_OK) {
             atomicMin(reinterpret_cast<unsigned long long*>(&acc[kAccBadReplica]), (unsigned long long)r);
@@ -132,13 +137,15 @@ __global__ void k_reduce(TraceDev t, unsigned long long* acc /* [kAccN] */) {
         }
     }
 #pragma unroll
-    for (int k = 0; k < 9; ++k) v[k] = warp_sum64(v[k]);
+    for (int k = 0; k < 11; ++k) v[k] = warp_sum64(v[k]);
     mx = __reduce_max_sync(0xFFFFFFFFu, mx);
     if ((threadIdx.x & 31) == 0) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (v[k]) atomicAdd(&acc[k], (unsigned long long)v[k]);
         if (v[8]) atomicAdd(&acc[kAccScanned], (unsigned long long)v[8]);
+        if (v[9]) atomicAdd(&acc[kAccPreempt], (unsigned long long)v[9]);
+        if (v[10]) atomicAdd(&acc[kAccForced], (unsigned long long)v[10]);
         atomicMax(&acc[kAccMaxPending], (unsigned long long)mx);
     }
 }

@@ -7,7 +7,7 @@ namespace tcm {
 // k_reduce accumulator layout (u64 each)
 enum : int {
     kAccIter = 0, kAccDecisions, kAccFF, kAccIdle, kAccSumPending, kAccDone, kAccReplicasDone,
-    kAccReplicasActive, kAccMaxPending, kAccBadReplica, kAccBadStatus, kAccScanned, kAccN
+    kAccReplicasActive, kAccMaxPending, kAccBadReplica, kAccBadStatus, kAccScanned, kAccPreempt, kAccForced, kAccN
 };
 
 void launch_init(const TraceDev& t, cudaStream_t s);

@@ -110,6 +110,15 @@ struct TraceDev {
     uint8_t* req_state;      // [N] stepwise engine: per-request class / phase byte
     ClassPack* kpack;        // [R] per-replica K1 class constants
     uint64_t* deadline;      // [N] stepwise engine, EDF: arrival*den + num*iso_e2e (set at ingest)
+    // stepwise engine, TCM_KV_GROWTH (NEXT-1, R28-R32)
+    uint32_t* kvres;         // [N] KV reserved at the last admission (footprint, or what a victim held)
+    uint32_t* kvfin;         // [N] KV held at the finish iteration (released by the calendar)
+    uint64_t* fin;           // [N] finish iteration of a decoding request
+    uint32_t* genp;          // [N] tokens generated when last preempted
+    uint64_t* pstart;        // [N] clock of the last preemption
+    uint32_t* pcount;        // [N] preemptions (result)
+    uint64_t* ptime;         // [N] preempted time (result)
+    uint32_t any_growth;     // some replica sets TCM_KV_GROWTH (from k_validate)
     FusedWs fw;              // fused engine only
 };
 

@@ -33,6 +33,9 @@ constexpr uint32_t ST_PARTIAL_OVERFLOW = 4;
 
 // request-state byte
 constexpr uint8_t RS_CLS = 3, RS_PEND = 4, RS_RES = 8, RS_FT = 16;
+// TCM_KV_GROWTH (NEXT-1): decoding, admitted before (a re-admission re-prefills what it held),
+// first token emitted
+constexpr uint8_t RS_DEC = 32, RS_PREV = 64, RS_GEN = 128;
 
 // stream staging: per warp, kStages chunks of 128 requests (1 KB arrivals + 128 B states)
 #ifndef TCM_SW_STAGES
@@ -149,8 +152,10 @@ struct Cal {
     uint32_t* occ;
 };
 
+// kvrel: KV released at the finish (footprint; TCM_KV_GROWTH: the final holding, and rs clears RS_DEC)
 __device__ __forceinline__ void cal_process(const Cal& c, uint32_t* link, uint64_t iter, uint64_t clock,
-                                            const uint32_t* fp, uint64_t* done, ReplicaState& st) {
+                                            const uint32_t* kvrel, uint64_t* done, ReplicaState& st,
+                                            uint8_t* rs = nullptr) {
     const uint32_t s = (uint32_t)(iter & (kCalSlots - 1));
     const uint32_t bit = 1u << (s & 31);
     const uint32_t w = c.occ[s >> 5];
@@ -159,7 +164,8 @@ __device__ __forceinline__ void cal_process(const Cal& c, uint32_t* link, uint64
     while (i != NIL) {
         const uint32_t ni = link[i];
         done[i] = clock;
-        st.kv_free += fp[i];
+        st.kv_free += kvrel[i];
+        if (rs) rs[i] = (uint8_t)(rs[i] & ~RS_DEC);
         st.n_dec--;
         st.done_count++;
         i = ni;
@@ -212,7 +218,7 @@ __device__ __forceinline__ void group_sync() {
 
 // Prologue (warp 0 of the group): ingest, idle jumps, decode-only fast-forward.
 // mode: 0 = nothing more this launch, 1 = decision iteration.
-template <int G>
+template <int G, bool GR>
 __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, GroupSmem<G>& sm, int lane) {
     ReplicaState st = t.state[r];
     const uint64_t base = t.offset[r];
@@ -223,6 +229,7 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
     uint8_t* rs = t.req_state + base;
     const bool prio = t.params[r].policy == TCM_POLICY_TCM;
     const bool edf = t.params[r].policy == TCM_POLICY_EDF;
+    const bool growth = GR && (t.params[r].flags & TCM_KV_GROWTH) != 0;
     int mode = 0;
     if (!(st.flags & FLAG_FINISHED) && st.head[1] > 0) {
         const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};
@@ -268,6 +275,10 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
                 st.idle_jumps++;
                 continue;
             }
+            if (growth && st.kv_free < st.n_dec) {       // R29: a preemption is due now
+                mode = 1;
+                break;
+            }
             if (lane == 0) {                             // Lemma L3 decode-only fast-forward
                 const uint64_t F = cal_next(cal, st.iter);
                 const uint64_t dt = m.c0 + m.cd * st.n_dec;
@@ -277,11 +288,18 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
                     j = ja < j ? ja : j;
                 }
                 j = j < st.head[1] ? j : st.head[1];
+                if (growth) {                            // R28: every iteration grows n_dec tokens
+                    const uint64_t jk = st.kv_free / st.n_dec;
+                    j = j < jk ? j : jk;
+                    st.kv_free -= j * st.n_dec;
+                }
                 st.clock += j * dt;
                 st.iter += j;
                 st.ff_iters += j;
                 st.head[1] -= (uint32_t)j;
-                if (st.iter == F) cal_process(cal, t.link + base, st.iter, st.clock, fp, t.done + base, st);
+                if (st.iter == F)
+                    cal_process(cal, t.link + base, st.iter, st.clock, growth ? t.kvfin + base : fp, t.done + base, st,
+                                growth ? rs : nullptr);
             }
             break;
         }
@@ -292,9 +310,119 @@ __device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, 
     }
 }
 
+// NEXT-1 (TCM_KV_GROWTH, readings R28-R32): before the order/admission of an iteration, while the
+// free KV cannot cover one decode token per decoding sequence, preempt the running request that
+// comes last (FCFS / EDF / naive aging: latest (arrival, id) = largest id; TCM: the
+// lowest (key, then largest id) among non-motorcycles, motorcycles only when nothing else runs,
+// SPEC.md:402).  The victim frees what it holds and waits again with rem = held (recomputation,
+// SPEC.md:87); then this iteration's decode tokens take their KV.  Warp-collective
+// on the group's first warp; st lives in shared memory.
+__device__ __noinline__ void sw_preempt(const ModelConst& m, const TraceDev& t, uint32_t r, uint64_t base, uint8_t* rs,
+                                        uint32_t* rem, bool prio, const K1Tables& tb, const ClassPack& kp,
+                                        ReplicaState& st, int lane) {
+    const uint32_t hi = st.nxt;
+    const uint64_t clock = st.clock;
+    const uint64_t* arr = t.arrival + base;
+    while (st.kv_free < st.n_dec) {
+        uint32_t v = NIL;
+        bool forced = false;
+        if (!prio) {
+            for (int64_t top = (int64_t)hi - 1; top >= 0 && v == NIL; top -= 32) {
+                const int64_t i = top - lane;
+                const bool run = i >= 0 && (rs[i] & (RS_RES | RS_DEC));
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, run);
+                if (b) v = (uint32_t)(top - (__ffs(b) - 1));
+            }
+        } else {
+            // advance the running-set lower bound past served requests
+            uint32_t lo = st.tail[0];
+            for (;;) {
+                const uint32_t i = lo + lane;
+                const bool stop = i >= hi || (rs[i] & (RS_PEND | RS_RES | RS_DEC));
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, stop);
+                if (b) {
+                    lo += __ffs(b) - 1;
+                    break;
+                }
+                lo += 32;
+            }
+            lo = lo < hi ? lo : hi;
+            if (lane == 0) st.tail[0] = lo;
+            for (int pass = 0; pass < 2 && v == NIL; ++pass) {
+                uint64_t bk = ~0ull;
+                uint32_t bi = NIL;
+                for (uint32_t c0 = lo; c0 < hi; c0 += 32) {
+                    const uint32_t i = c0 + lane;
+                    const uint8_t sb = i < hi ? rs[i] : 0;
+                    const int c = sb & RS_CLS;
+                    if ((sb & (RS_RES | RS_DEC)) && (pass == 1 || c != 0)) {
+                        const uint64_t k = k1_key_bf(kp.S[c], kp.p[c], kp.C[c], (kp.zero_mask >> c) & 1u, clock - arr[i], tb);
+                        if (k < bk || (k == bk && (bi == NIL || i > bi))) {
+                            bk = k;
+                            bi = i;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {           // warp arg-min (key asc, id desc)
+                    const uint64_t ok = __shfl_xor_sync(0xFFFFFFFFu, bk, o);
+                    const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+                    if (oi != NIL && (bi == NIL || ok < bk || (ok == bk && oi > bi))) {
+                        bk = ok;
+                        bi = oi;
+                    }
+                }
+                v = bi;
+                forced = pass == 1;
+            }
+        }
+        if (lane == 0 && v != NIL) {
+            const uint8_t sb = rs[v];
+            uint32_t held;
+            if (sb & RS_DEC) {
+                const uint64_t F = t.fin[base + v];
+                const uint32_t togo = (uint32_t)(F - st.iter);
+                held = t.kvfin[base + v] - togo;
+                t.genp[base + v] = (uint32_t)t.out[base + v] - togo;
+                // unlink from its calendar slot
+                const uint32_t slot = (uint32_t)(F & (kCalSlots - 1));
+                uint32_t* cal = t.cal + (size_t)r * kCalSlots;
+                uint32_t* link = t.link + base;
+                uint32_t prv = NIL, cur = cal[slot];
+                while (cur != v) {
+                    prv = cur;
+                    cur = link[cur];
+                }
+                if (prv == NIL) cal[slot] = link[v];
+                else link[prv] = link[v];
+                if (cal[slot] == NIL) t.occ[(size_t)r * kCalWords + (slot >> 5)] &= ~(1u << (slot & 31));
+                st.n_dec--;
+                st.n_pend++;
+                rs[v] = (uint8_t)((sb & ~RS_DEC) | RS_PEND);
+            } else {                                         // a partial prefill
+                held = t.kvres[base + v];
+                rs[v] = (uint8_t)(sb & ~RS_RES);
+            }
+            rem[v] = held;
+            st.kv_free += held;
+            t.pcount[base + v]++;
+            t.pstart[base + v] = clock;
+            st.tail[1]++;
+            if (forced) st.tail[2]++;
+            if (v < st.head[0]) st.head[0] = v;
+        }
+        __syncwarp();
+        if (v == NIL) break;                                 // unreachable: n_dec > 0
+    }
+    if (lane == 0) st.kv_free -= st.n_dec;                   // this iteration's decode tokens
+    __syncwarp();
+}
+
 }  // namespace
 
-template <int G>
+// GR: some replica of the trace runs TCM_KV_GROWTH (NEXT-1); the plain instantiation compiles
+// the growth code out of the hot path.
+template <int G, bool GR>
 __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
                                                       int count_active) {
     constexpr int kGroups = kWarpsPerBlock / G;
@@ -316,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
     const K1Tables tb{s_lnR, s_lnT, s_expT};
 
     for (uint32_t r = blockIdx.x * kGroups + group; r < t.R; r += gridDim.x * kGroups) {
-        if (wg == 0) sw_prologue<G>(m, t, r, sm, lane);
+        if (wg == 0) sw_prologue<G, GR>(m, t, r, sm, lane);
         group_sync<G>();
         if (sm.mode == 0) {
             if (wg == 0 && lane == 0) {
@@ -340,13 +468,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
         uint8_t* rs = t.req_state + base;
         uint32_t* rem = remv + base;
         const uint64_t clock = sm.st.clock;
-        const uint32_t lo = sm.st.head[0], hi = sm.st.nxt;
+        const bool growth = GR && (prm.flags & TCM_KV_GROWTH) != 0;
         if (wg == 0) {
             {   // stage the replica's ClassPack (144 B) in shared memory
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(t.kpack + r);
                 uint32_t* dst = reinterpret_cast<uint32_t*>(&sm.kp);
                 for (int q = lane; q < (int)(sizeof(ClassPack) / 4); q += 32) dst[q] = src[q];
             }
+            __syncwarp();
+            if (growth) sw_preempt(m, t, r, base, rs, rem, prio, tb, sm.kp, sm.st, lane);
             if (lane == 0) {
                 const uint32_t B = prm.chunk_budget;
                 sm.left = B > sm.st.n_dec ? B - sm.st.n_dec : 0;     // R8
@@ -359,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
             }
         }
         group_sync<G>();
+        const uint32_t lo = sm.st.head[0], hi = sm.st.nxt;     // after any preemption (NEXT-1)
         const bool filter_ok = sm.kp.filter_ok != 0;
         // compound sort keys need every key in [1e-12, 2^17): P <= Smax_c
         const bool cmp_ok = prio && sm.kp.Smax[0] < 65536.0 && sm.kp.Smax[1] < 65536.0 && sm.kp.Smax[2] < 65536.0;
@@ -692,12 +823,14 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 const uint64_t kv = sm.st.kv_free;
                 const bool blocked_prev = sm.blocked;
                 uint32_t f = 0, rr = 0, il = 0;
-                bool res = false;
+                bool res = false, prev = false;
                 if (valid) {
-                    f = fp[li];
-                    res = (rsc[li] & RS_RES) != 0;
-                    rr = res ? rem[li] : f;
-                    il = res ? 0 : inl[li];
+                    const uint8_t sb = rsc[li];
+                    res = (sb & RS_RES) != 0;
+                    prev = (sb & RS_PREV) != 0;          // NEXT-1 re-admission (R30)
+                    rr = (res || prev) ? rem[li] : fp[li];
+                    f = prev ? rr : fp[li];              // KV to reserve
+                    il = (res || prev) ? 0 : inl[li];
                 }
                 const bool waiting = valid && !res;
                 bool kv_ok;
@@ -724,11 +857,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 const uint64_t chunk = (part && reached) ? (rr < left - excl ? rr : left - excl) : 0;
                 const bool admitted = kv_ok && reached;
                 const bool misfit = !skip && waiting && !blocked_prev && !kv_ok && reached;
-                const uint32_t adm_mask = __ballot_sync(0xFFFFFFFFu, admitted);
+                const uint32_t adm_mask = __ballot_sync(0xFFFFFFFFu, admitted && !prev);   // first admissions
                 const uint32_t rank = __popc(adm_mask & ((1u << lane) - 1));
                 if (admitted) {
-                    t.admit_seq[base + li] = sm.st.seq + rank;
-                    rs[li] = (uint8_t)(rsc[li] | RS_RES);
+                    if (!prev) t.admit_seq[base + li] = sm.st.seq + rank;
+                    rs[li] = (uint8_t)(rsc[li] | RS_RES | (growth ? RS_PREV : 0));
+                    if (growth) {
+                        t.kvres[base + li] = f;
+                        if (prev) t.ptime[base + li] += clock - t.pstart[base + li];   // R31
+                    }
                 }
                 if (chunk > 0) {
                     const uint32_t nr = rr - (uint32_t)chunk;
@@ -819,7 +956,8 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 st.sum_pending += st.n_pend;
                 st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
                 const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};
-                cal_process(cal, t.link + base, st.iter, st.clock, fp, t.done + base, st);
+                cal_process(cal, t.link + base, st.iter, st.clock, growth ? t.kvfin + base : fp, t.done + base, st,
+                            growth ? rs : nullptr);
             }
             __syncwarp();
             const uint64_t now = st.clock;
@@ -831,6 +969,29 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
             uint32_t* link = t.link + base;
             uint64_t kv_add = 0, n_dec_add = 0, done_add = 0;
             auto stamp = [&](uint32_t i) {
+                if (growth) {                       // NEXT-1: first token once; a re-prefill emits the next
+                    const uint8_t sb = rs[i];
+                    if (!(sb & RS_GEN)) t.first_token[base + i] = now;
+                    const uint32_t o = out[i];
+                    const uint32_t ga = t.genp[base + i] + 1;
+                    const uint32_t kr = t.kvres[base + i];
+                    if (ga >= o) {
+                        t.done[base + i] = now;
+                        kv_add += kr;
+                        done_add++;
+                        rs[i] = (uint8_t)((sb & ~(RS_PEND | RS_FT | RS_RES)) | RS_GEN);
+                    } else {
+                        const uint64_t F = it + (o - ga);
+                        t.fin[base + i] = F;
+                        t.kvfin[base + i] = kr + (o - ga);
+                        const uint32_t slot = (uint32_t)(F & (kCalSlots - 1));
+                        link[i] = atomicExch(&cal[slot], i);
+                        atomicOr(&occ[slot >> 5], 1u << (slot & 31));
+                        n_dec_add++;
+                        rs[i] = (uint8_t)((sb & ~(RS_PEND | RS_FT | RS_RES)) | RS_GEN | RS_DEC);
+                    }
+                    return;
+                }
                 t.first_token[base + i] = now;
                 rs[i] = (uint8_t)(rs[i] & ~(RS_PEND | RS_FT | RS_RES));
                 const uint32_t o = out[i];
@@ -893,6 +1054,9 @@ __global__ void k_sw_init(TraceDev t) {
     if (r < t.R) {
         t.state[r].head[0] = 0;
         t.state[r].head[1] = 0;
+        t.state[r].tail[0] = 0;      // NEXT-1: running-set lower bound, preemptions, forced ones
+        t.state[r].tail[1] = 0;
+        t.state[r].tail[2] = 0;
     }
 }
 
@@ -921,10 +1085,12 @@ Launch stepwise_config(uint32_t R) {
     int dev = 0, sms = 148, per_sm1 = 1, per_sm8 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1>, kThreads, kRingBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8>, kThreads, kRingBytes);
+    cudaFuncSetAttribute(k_step<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1, false>, kThreads, kRingBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8, false>, kThreads, kRingBytes);
     if (per_sm1 < 1) per_sm1 = 1;
     if (per_sm8 < 1) per_sm8 = 1;
     // Warp per replica when there are enough replicas to fill every warp slot twice over;
@@ -964,8 +1130,13 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         if (cudaEventRecord(ev_begin, s) != cudaSuccess) return TCM_E_CUDA;
         for (uint32_t q = 0; q < this_chunk; ++q) {
             const int last = q + 1 == this_chunk;
-            if (L.group == 1) k_step<1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
-            else k_step<8><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+            if (t.any_growth) {
+                if (L.group == 1) k_step<1, true><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+                else k_step<8, true><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+            } else {
+                if (L.group == 1) k_step<1, false><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+                else k_step<8, false><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+            }
             (*launches)++;
         }
         done_launches += this_chunk;

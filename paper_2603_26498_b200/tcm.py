@@ -15,12 +15,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TCM_LIB_PATH") or os.path.join(_HERE, "_build", "libtcm.so")
 
-TCM_ABI_VERSION = 2
+TCM_ABI_VERSION = 3
 TCM_OK = 0
 ERRORS = {-1: "TCM_E_ARG", -2: "TCM_E_STATE", -3: "TCM_E_CAPACITY", -4: "TCM_E_CUDA",
           -5: "TCM_E_OOM", -6: "TCM_E_REPLICA", -7: "TCM_E_VERSION"}
 POLICY_FCFS, POLICY_TCM, POLICY_EDF, POLICY_NAIVE_AGING = 0, 1, 2, 3
 ADMIT_SKIP = 1
+KV_GROWTH = 2          # NEXT-1: decode KV growth + preemption by recomputation (R28-R32)
 ENGINE_FUSED, ENGINE_STEPWISE = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 HIST_BINS, GROUPS, NCNT = 496, 4, 6
@@ -61,6 +62,7 @@ class tcm_results_view(ctypes.Structure):
     _fields_ = [
         ("mem", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("admit_seq", ctypes.c_void_p),
         ("first_token_us", ctypes.c_void_p), ("done_us", ctypes.c_void_p),
+        ("preempt_count", ctypes.c_void_p), ("preempted_us", ctypes.c_void_p),
     ]
 
 
@@ -69,7 +71,8 @@ class tcm_stats_host(ctypes.Structure):
         "iterations", "decisions", "ff_iterations", "idle_jumps", "sum_pending", "max_pending",
         "requests_done", "replicas_done", "replicas_active", "kernel_launches", "scanned_decisions")] + [
         ("first_bad_replica", ctypes.c_int32), ("first_bad_status", ctypes.c_int32),
-        ("reset_ms", ctypes.c_double), ("engine_ms", ctypes.c_double), ("stamp_ms", ctypes.c_double)]
+        ("reset_ms", ctypes.c_double), ("engine_ms", ctypes.c_double), ("stamp_ms", ctypes.c_double),
+        ("preemptions", ctypes.c_uint64), ("forced_preemptions", ctypes.c_uint64)]
 
 
 # tcm_replica_params (32 B) as a numpy record so whole sweeps are built vectorised.
@@ -183,6 +186,8 @@ def tcm_load_trace(ctx, trace: dict, results: dict | None, mem=MEM_DEVICE):
         rv.admit_seq = _ptr(results.get("admit_seq"))
         rv.first_token_us = _ptr(results.get("first_token_us"))
         rv.done_us = _ptr(results.get("done_us"))
+        rv.preempt_count = _ptr(results.get("preempt_count"))
+        rv.preempted_us = _ptr(results.get("preempted_us"))
     _check(lib().tcm_load_trace(ctx, ctypes.byref(tv), ctypes.byref(rv)), ctx)
 
 
@@ -275,11 +280,15 @@ def to_device_params(params: np.ndarray, device="cuda"):
     return torch.from_numpy(np.ascontiguousarray(params, dtype=PARAMS_DTYPE).view(np.uint8)).to(device)
 
 
-def alloc_results(n: int, device="cuda") -> dict:
+def alloc_results(n: int, device="cuda", preemption: bool = False) -> dict:
     import torch
-    return {"admit_seq": torch.empty(n, dtype=torch.uint32, device=device),
-            "first_token_us": torch.empty(n, dtype=torch.uint64, device=device),
-            "done_us": torch.empty(n, dtype=torch.uint64, device=device)}
+    res = {"admit_seq": torch.empty(n, dtype=torch.uint32, device=device),
+           "first_token_us": torch.empty(n, dtype=torch.uint64, device=device),
+           "done_us": torch.empty(n, dtype=torch.uint64, device=device)}
+    if preemption:     # NEXT-1 outputs (stepwise engine with KV_GROWTH replicas)
+        res["preempt_count"] = torch.empty(n, dtype=torch.uint32, device=device)
+        res["preempted_us"] = torch.empty(n, dtype=torch.uint64, device=device)
+    return res
 
 
 def generate_device(reps: np.ndarray, device="cuda", stream=None) -> dict:
