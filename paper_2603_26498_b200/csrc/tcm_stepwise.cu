@@ -28,6 +28,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr int kTop = 32;
+constexpr int kItersPerLaunch = 16;   // engine iterations per replica per k_step launch (tcm_run)
 constexpr int kMaxPart = 32;
 constexpr uint32_t ST_PARTIAL_OVERFLOW = 4;
 
@@ -444,15 +445,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
     const K1Tables tb{s_lnR, s_lnT, s_expT};
 
     for (uint32_t r = blockIdx.x * kGroups + group; r < t.R; r += gridDim.x * kGroups) {
+      // up to kItersPerLaunch engine iterations of this replica per launch (each one the full
+      // a1-a5 step); tcm_step's budget (head[1]) still bounds the total
+      for (int kit = 0; kit < kItersPerLaunch; ++kit) {
         if (wg == 0) sw_prologue<G, GR>(m, t, r, sm, lane);
         group_sync<G>();
         if (sm.mode == 0) {
-            if (wg == 0 && lane == 0) {
-                t.state[r] = sm.st;
-                if (count_active && !(sm.st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
-            }
+            if (wg == 0 && lane == 0) t.state[r] = sm.st;
             group_sync<G>();
-            continue;
+            break;
         }
 
         const tcm_replica_params prm = t.params[r];
@@ -1035,9 +1036,11 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 st.n_pend -= (uint32_t)nd;
                 st.head[0] = l2 < hi ? l2 : hi;
                 t.state[r] = st;
-                if (count_active && !(st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
             }
         }
+        group_sync<G>();
+      }
+        if (wg == 0 && lane == 0 && count_active && !(sm.st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
         group_sync<G>();
     }
 }

@@ -58,12 +58,13 @@ def _grid(name, cells, replicas_per_cell, n_requests, seed, replica_ids):
     params = tcm.make_params(R)
     for j, g in enumerate(replica_ids):
         c = cells[g % nc]
-        gen[j] = T.make_replica(seed, int(g), n_requests, c["rate"], c["mix"], c["kv"])
+        gen[j] = T.make_replica(seed, int(g), n_requests, c["rate"], c["mix"], c.get("gen_kv", c["kv"]))
         params[j]["policy"] = c["policy"]
         params[j]["kv_capacity"] = c["kv"]
         params[j]["aging_alpha"] = c["alpha"]
         params[j]["chunk_budget"] = c["budget"]
         params[j]["cell_id"] = g % nc
+        params[j]["flags"] = c.get("flags", 0)
     return Sweep(name, gen, params, nc, cells)
 
 
@@ -97,6 +98,15 @@ def c4(rank=0, world=1, replicas_per_gpu=65536, n_requests=10_000, seed=4044):
     cells = c4_cells()
     seeds_total = replicas_per_gpu * world // len(cells)
     return _grid("C4", cells, seeds_total, n_requests, seed, rank_ids(len(cells), seeds_total, rank, world))
+
+
+def c4_growth(rank=0, world=1, replicas_per_gpu=4096, n_requests=2000, seed=4045):
+    """NEXT-1 memory-pressure sweep: the C4 cells with decode KV growth and preemption
+    (tcm.KV_GROWTH, readings R28-R32) on the stepwise engine.  Footprints are clamped to
+    kv - 2048 so that footprint + out - 1 fits the KV capacity (R28)."""
+    cells = [dict(c, gen_kv=c["kv"] - 2048, flags=tcm.KV_GROWTH) for c in c4_cells()]
+    seeds_total = replicas_per_gpu * world // len(cells)
+    return _grid("C4-growth", cells, seeds_total, n_requests, seed, rank_ids(len(cells), seeds_total, rank, world))
 
 
 def c5_cells():
