@@ -306,6 +306,10 @@ def run_tcm(args, rank, world, local):
         out["roofline_step"] = st_res.pop("C2'")
         out["step_kernels"] = st_res
 
+    if not args.skip_next1 and rank == 0:
+        out["next1"] = bench_next1(args, dev, stream)
+        log("next1 done")
+
     # end-to-end through the C ABI with HOST buffers (H2D + run + D2H inside the timed region)
     log("stepwise done")
     if not args.skip_e2e:
@@ -344,7 +348,9 @@ def _stage_c2(replicas, pending, engine, dev, stream):
 
 
 def time_steps(sim, stream, iters, reps):
-    """Device time of single engine iterations 2..iters+1 (iteration 1 runs request 0 alone).
+    """Device time of single steady-state engine iterations 3..iters+2 (iteration 1 runs request 0
+    alone, iteration 2 also ingests every other request: its classify bytes are not in the
+    9 B-per-pending figure, so it is not timed).
     Returns (kernel ms, call ms, pending): the kernel time is the library's own CUDA-event
     measurement around its k_step / k_fused launch on its stream (tcm_stats_host.engine_ms);
     the call time brackets the whole tcm_step call (budget kernel, memsets, active-count read)."""
@@ -352,7 +358,8 @@ def time_steps(sim, stream, iters, reps):
     times, calls, pend = [], [], []
     for rep in range(reps):
         sim.reset()
-        sim.step(1)
+        sim.step(1)          # iteration 1: request 0 alone (its 60 s encode moves the clock past every arrival)
+        sim.step(1)          # iteration 2: ingests + classifies the other requests (a1), then decides
         for _ in range(iters):
             s0 = sim.stats()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -407,6 +414,55 @@ def bench_stepwise(args, dev, stream):
     lat["pending"] = keys
     out["C2_latency"] = lat
     return out
+
+
+def bench_next1(args, dev, stream):
+    """NEXT-1 (decode KV growth + preemption by recomputation, R28-R32) on the stepwise engine:
+    the C4 cells with tcm.KV_GROWTH at a reduced size; simulated requests/s, preemptions and the
+    motorcycle share of the victims per policy (fig:preemptions)."""
+    import torch
+    from paper_2603_26498_b200 import tcm
+    from paper_2603_26498_b200 import workloads as W
+    sw = W.c4_growth(replicas_per_gpu=args.next1_replicas, n_requests=args.next1_requests)
+    with torch.cuda.stream(stream):
+        tr = tcm.generate_device(sw.gen, device=dev, stream=stream)
+        tr["params"] = torch.from_numpy(sw.params.view(np.uint8)).to(dev)
+        res = tcm.alloc_results(sw.n_requests, device=dev, preemption=True)
+    stream.synchronize()
+    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE, n_cells=sw.n_cells), stream)
+    sim.load(tr, res)
+    times = []
+    for rep in range(2):                       # the first run is warm-up
+        sim.reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.run()
+        e1.record(stream)
+        stream.synchronize()
+        times.append(e0.elapsed_time(e1))
+    st = sim.stats()
+    ms = times[-1]
+    # per-policy victim classes (R13 smart thresholds: text < 4096 tokens is a motorcycle)
+    pc = res["preempt_count"].cpu().numpy()
+    fp = tr["footprint"].cpu().numpy().view(np.uint32)
+    md = tr["modality"].cpu().numpy()
+    off = tr["req_offset"].cpu().numpy().astype(np.int64)
+    pol = np.repeat(sw.params["policy"], np.diff(off))
+    moto = (md == 0) & (fp < 4096)
+    by = {}
+    for name, p in (("FCFS", tcm.POLICY_FCFS), ("TCM", tcm.POLICY_TCM)):
+        sel = pol == p
+        by[name] = {"preemptions": int(pc[sel].sum()), "motorcycle_preemptions": int(pc[sel & moto].sum()),
+                    "requests_preempted": int((pc[sel] > 0).sum())}
+    sim.close()
+    return {"workload": f"C4-growth: {sw.n_replicas} replicas x {args.next1_requests} requests (C4 cells, "
+                        "KV growth + preemption), stepwise engine",
+            "value": sw.n_requests / (ms / 1e3), "unit": "requests/s", "ms": ms,
+            "decisions_per_s": st["decisions"] / (ms / 1e3), "iterations": st["iterations"],
+            "preemptions": st["preemptions"], "forced_preemptions": st["forced_preemptions"],
+            "by_policy": by,
+            "note": "bounded by the heaviest replica's serial iteration chain (no closed-form fast-forward "
+                    "under KV growth); DESIGN.md 9"}
 
 
 def bench_e2e(args, sw, trace, dev, stream, dist, world):
@@ -473,6 +529,9 @@ def main():
     ap.add_argument("--step-iters", type=int, default=4)
     ap.add_argument("--step-reps", type=int, default=3)
     ap.add_argument("--skip-step", action="store_true")
+    ap.add_argument("--skip-next1", action="store_true")
+    ap.add_argument("--next1-replicas", type=int, default=1024)
+    ap.add_argument("--next1-requests", type=int, default=1000)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
