@@ -119,7 +119,7 @@ def _oracle_job(job):
     return dt, n, r.counters["decisions"]
 
 
-def oracle_sample(sweep, n_trunc=1000, per_cell=1):
+def oracle_sample(sweep, n_trunc=1000, per_cell=1, cells_sel=None):
     """Time the oracle (as it stands) on a bounded sample of the sweep: `per_cell` replicas of
     every cell, truncated to their first n_trunc requests, one replica per process on the host
     cores."""
@@ -127,7 +127,7 @@ def oracle_sample(sweep, n_trunc=1000, per_cell=1):
     R = sweep.n_replicas
     cells = sweep.params["cell_id"]
     idx = []
-    for c in range(sweep.n_cells):
+    for c in (range(sweep.n_cells) if cells_sel is None else cells_sel):
         idx.extend(np.nonzero(cells == c)[0][:per_cell].tolist())
     jobs = [(sweep.gen[i], int(sweep.params[i]["policy"]), int(sweep.params[i]["kv_capacity"]),
              float(sweep.params[i]["aging_alpha"]), int(sweep.params[i]["chunk_budget"]), n_trunc) for i in idx]
@@ -190,13 +190,17 @@ def run_tcm(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
 
-    sw = W.c4(rank, world, replicas_per_gpu=args.replicas, n_requests=args.requests)
+    if args.workload == "c5":
+        # C5 (BASELINE.json configs[4]): 1M replicas on 8 GPUs = 131,072 per GPU (weak scaling)
+        sw = W.c5(rank, world, replicas=args.replicas * world, n_requests=args.requests)
+    else:
+        sw = W.c4(rank, world, replicas_per_gpu=args.replicas, n_requests=args.requests)
     R, N = sw.n_replicas, sw.n_requests
-    log(f"rank {rank}: C4 shard {R} replicas, {N} requests; generating on device")
+    log(f"rank {rank}: {args.workload.upper()} shard {R} replicas, {N} requests; generating on device")
     with torch.cuda.stream(stream):
         trace = tcm.generate_device(sw.gen, device=dev, stream=stream)
         trace["params"] = torch.from_numpy(sw.params.view(np.uint8)).to(dev)
-        results = tcm.alloc_results(N, device=dev)
+        results = tcm.alloc_results(N, device=dev) if args.workload == "c4" else None
     stream.synchronize()
     cfg = tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells)
     sim = tcm.Simulation(cfg, stream)
@@ -275,14 +279,20 @@ def run_tcm(args, rank, world, local):
         except Exception:
             traffic = None
 
+    if args.workload == "c5":
+        wl = (f"C5 full policy sweep: {R} replicas x {args.requests} requests per GPU (16 lambda x 8 mixes x 16 alpha x "
+              f"8 chunk budgets = {sw.n_cells} cells x seeds; 1M replicas at 8 GPUs), fused engine, per-request results "
+              "kept in the library workspace")
+    else:
+        wl = (f"C4 memory-pressure sweep: {args.replicas} replicas x {args.requests} requests per GPU "
+              "(50/20/30 mix, KV 128k..16k x lambda 0.5..4 x FCFS/TCM), fused engine")
     out = {
-        "metric": "simulated requests/sec (C4 memory-pressure sweep); decisions/sec alongside",
+        "metric": f"simulated requests/sec ({args.workload.upper()} sweep); decisions/sec alongside",
         "value": req_s, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
         "decisions_per_s": dec_s,
-        "config": {"workload": f"C4 memory-pressure sweep: {args.replicas} replicas x {args.requests} requests per GPU "
-                               "(50/20/30 mix, KV 128k..16k x lambda 0.5..4 x FCFS/TCM), fused engine",
+        "config": {"workload": wl, "n_cells": sw.n_cells,
                    "replicas_per_gpu": args.replicas, "requests_per_replica": args.requests,
                    "requests_per_step": int(tot[0] / args.steps), "parallelism": f"replicas sharded x{world}",
                    "l2": "inputs larger than L2 (trace %.1f GB per GPU)" % (N * 19 / 1e9)},
@@ -317,11 +327,12 @@ def run_tcm(args, rank, world, local):
     log("e2e done")
 
     if rank == 0 and not args.skip_cpu:
-        s = oracle_sample(sw, n_trunc=args.ref_requests)
+        sel = None if sw.n_cells <= 64 else list(range(0, sw.n_cells, sw.n_cells // 32))   # C5: 32 spread cells
+        s = oracle_sample(sw, n_trunc=args.ref_requests, cells_sel=sel)
         out["cpu_baseline"] = {"value": s["requests"] / s["wall_s"], "unit": "requests/s", "cores": s["cores"],
                                "kind": "oracle",
                                "decisions_per_s": s["decisions"] / s["wall_s"],
-                               "sample": f"{s['replicas']} C4 replicas (one per cell), first "
+                               "sample": f"{s['replicas']} {args.workload.upper()} replicas (one per sampled cell), first "
                                          f"{s['n_trunc']} requests each, one oracle process per replica, "
                                          f"{s['wall_s']:.1f} s wall"}
     sim.close()
@@ -521,7 +532,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["tcm", "reference"], default="tcm")
-    ap.add_argument("--replicas", type=int, default=65536, help="C4 replicas per GPU")
+    ap.add_argument("--workload", choices=["c4", "c5"], default="c4")
+    ap.add_argument("--replicas", type=int, default=None, help="replicas per GPU (C4 65,536; C5 131,072)")
     ap.add_argument("--requests", type=int, default=10_000)
     ap.add_argument("--ref-requests", type=int, default=2000, help="oracle sample: requests per replica")
     ap.add_argument("--step-replicas", type=int, default=65536)
@@ -535,6 +547,11 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
+    if args.replicas is None:
+        args.replicas = 131072 if args.workload == "c5" else 65536
+    if args.workload == "c5":
+        # the C5 step moves 51 GB of per-request data; its e2e leg and the C4-specific legs are not run
+        args.skip_e2e = args.skip_step = args.skip_next1 = True
     rank, world, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
