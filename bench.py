@@ -323,7 +323,13 @@ def run_tcm(args, rank, world, local):
     # end-to-end through the C ABI with HOST buffers (H2D + run + D2H inside the timed region)
     log("stepwise done")
     if not args.skip_e2e:
-        out["e2e"] = bench_e2e(args, sw, trace, dev, stream, dist, world)
+        # free the device-resident run first: the two e2e contexts need ~74 GB each
+        host = host_copy(trace)
+        sim.close()
+        del trace, results
+        torch.cuda.empty_cache()
+        out["e2e"] = bench_e2e(args, sw, host, dev, dist, world)
+        del host
     log("e2e done")
 
     if rank == 0 and not args.skip_cpu:
@@ -476,48 +482,86 @@ def bench_next1(args, dev, stream):
                     "under KV growth); DESIGN.md 9"}
 
 
-def bench_e2e(args, sw, trace, dev, stream, dist, world):
-    """Same metric through the C ABI with HOST (pinned) buffers: every step copies the trace in,
-    runs, copies per-request results back and reads the a6 counters."""
+def host_copy(trace):
+    """Pinned host copies of the device trace (the e2e leg's inputs)."""
+    return {k: trace[k].cpu().pin_memory()
+            for k in ("req_offset", "arrival_us", "footprint", "inline_us", "out_tokens", "modality", "params")}
+
+
+def bench_e2e(args, sw, host, dev, dist, world):
+    """Same metric through the C ABI with HOST (pinned) buffers: every step copies its trace in
+    (tcm_load_trace), runs (tcm_run, which copies the per-request results back) and reads the a6
+    counters (tcm_stats).  Two contexts on two streams, each driven by its own host thread, take
+    alternate steps, so one step's host<->device copies overlap the other step's kernels (a user
+    streaming sweeps through the API does the same); the timed region covers every step's copies."""
+    import threading
     import torch
     from paper_2603_26498_b200 import tcm
     N = sw.n_requests
-    host = {}
-    for k in ("req_offset", "arrival_us", "footprint", "inline_us", "out_tokens", "modality", "params"):
-        t = trace[k].cpu().pin_memory()
-        host[k] = t
-    res = {"admit_seq": torch.empty(N, dtype=torch.uint32).pin_memory(),
-           "first_token_us": torch.empty(N, dtype=torch.uint64).pin_memory(),
-           "done_us": torch.empty(N, dtype=torch.uint64).pin_memory()}
     h2d = sum(v.numel() * v.element_size() for v in host.values())
-    d2h = sum(v.numel() * v.element_size() for v in res.values())
-    cfg = tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells)
-    sim = tcm.Simulation(cfg, stream)
-    steps = max(1, min(args.steps, 2))
+    per_ctx = max(2, min(args.steps, 4) // 2)
+    lanes = []
+    for _ in range(2):
+        res = {"admit_seq": torch.empty(N, dtype=torch.uint32).pin_memory(),
+               "first_token_us": torch.empty(N, dtype=torch.uint64).pin_memory(),
+               "done_us": torch.empty(N, dtype=torch.uint64).pin_memory()}
+        st = torch.cuda.Stream(device=dev)
+        sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells), st)
+        lanes.append((sim, res, st))
+    d2h = sum(v.numel() * v.element_size() for v in lanes[0][1].values())
 
-    def step():
+    def step(lane):
+        sim, res, st = lane
         sim.load(host, res, mem=tcm.MEM_HOST)     # H2D inside the timed region
         sim.run()                                 # results copied back (D2H) before returning
         hist, cnt, _ = sim.aggregate(device=dev)
         return cnt
 
-    step()                                        # warm-up
+    for lane in lanes:                            # warm-up (allocates each context's workspace)
+        step(lane)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    loaded = threading.Event()
+    errors = []
+
+    def worker(k):
+        try:
+            torch.cuda.set_device(dev)
+            if k == 1:
+                loaded.wait()                     # stagger: context 1 starts once context 0 has its inputs
+            for i in range(per_ctx):
+                sim, res, st = lanes[k]
+                sim.load(host, res, mem=tcm.MEM_HOST)
+                if k == 0 and i == 0:
+                    loaded.set()
+                sim.run()
+                sim.aggregate(device=dev)
+        except Exception as e:                    # surfaced below
+            errors.append(e)
+            loaded.set()
+
     t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
+    if errors:
+        raise errors[0]
     mx = torch.tensor([wall], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    sim.close()
+    for sim, _, _ in lanes:
+        sim.close()
+    steps = 2 * per_ctx
     total_req = N * world * steps
     return {"value": total_req / float(mx[0]), "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "note": "HOST pinned buffers through tcm_load_trace/tcm_run/tcm_stats; host wall clock, max over ranks"}
+            "note": "HOST pinned buffers through tcm_load_trace/tcm_run/tcm_stats every step; two contexts on two "
+                    "streams take alternate steps so copies overlap kernels; host wall clock, max over ranks"}
 
 
 def log(*a):
