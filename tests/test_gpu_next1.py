@@ -140,3 +140,30 @@ def test_growth_rejections():
     with pytest.raises(tcm.TcmError) as e:
         run_gpu(tr, params)
     assert e.value.code == -3
+
+
+def test_growth_edge_cases():
+    # empty replica, a lone request, out = 1 everywhere (no growth), B = 1, KV exactly f + out - 1
+    reqs = [
+        [],
+        [[0, 100, 0, 1, 0]],
+        [[0, 50, 0, 1, 0], [0, 60, 0, 1, 1], [5, 70, 0, 1, 2]],
+        [[0, 8, 0, 5, 0], [0, 10, 0, 3, 0], [1, 4, 0, 4, 1]],
+        [[0, 200, 0, 301, 0]],
+        [[0, 3, 0, 8, 0], [0, 3, 0, 6, 1]],
+    ]
+    kvs = [100, 100, 100, 14, 500, 16]
+    budgets = [2048, 2048, 1, 1, 2048, 2]
+    tr = T.concat([T.from_requests(r) for r in reqs]) if hasattr(T, "concat") else None
+    if tr is None:
+        pytest.skip("tracegen.concat not available")
+    params = tcm.make_params(len(reqs))
+    params["kv_capacity"] = kvs
+    params["chunk_budget"] = budgets
+    params["flags"] = tcm.KV_GROWTH
+    for pol in (tcm.POLICY_FCFS, tcm.POLICY_TCM):
+        params["policy"] = pol
+        out, st = run_gpu(tr, params)
+        c = check(tr, params, out, range(len(reqs)))
+        assert st["requests_done"] == tr.n_requests
+        assert c["preemptions"] > 0 and st["preemptions"] == c["preemptions"]
