@@ -564,7 +564,8 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 amx = am0 > am1 ? am0 : am1;
                 amx = amx > am2 ? amx : am2;
             };
-            int qn = 0;
+            int qn = 0, qh = 0;                      // refine queue: count and ring head
+            constexpr int kQ = GroupSmem<G>::kQ;
             uint32_t* qid = sm.qid[wg];
             uint64_t* qw = sm.qw[wg];
             uint8_t* qc = sm.qc[wg];
@@ -640,9 +641,11 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 int cc = 0;
                 uint64_t qwl = 0;
                 if (lane < cnt) {
-                    id = qid[lane];
-                    cc = qc[lane];
-                    qwl = qw[lane];
+                    int q = qh + lane;                                 // ring slot
+                    q -= q >= kQ ? kQ : 0;
+                    id = qid[q];
+                    cc = qc[q];
+                    qwl = qw[q];
                     // the limits may have tightened since this request was queued.  The queue is
                     // not in id order within a chunk, so a tie class is decided by id here.
                     const int qcl = cc & RS_CLS;
@@ -762,43 +765,24 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                     const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, nq & 2u);
                     const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, nq & 4u);
                     const uint32_t lt = (1u << lane) - 1u;
-                    int pos = qn + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+                    int pos = qh + qn + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         if ((qbits >> j) & 1u) {
                             const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                            qid[pos] = (uint32_t)(e0 + j);
-                            qw[pos] = clock - a4[j];
-                            qc[pos] = (uint8_t)((sb & RS_CLS) | (sb & RS_RES));
+                            const int q = pos >= kQ ? pos - kQ : pos;  // ring slot (pos < 2 kQ)
+                            qid[q] = (uint32_t)(e0 + j);
+                            qw[q] = clock - a4[j];
+                            qc[q] = (uint8_t)((sb & RS_CLS) | (sb & RS_RES));
                             ++pos;
                         }
                     }
                     qn += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
                     __syncwarp();
-                    while (qn >= 32) {
+                    while (qn >= 32) {                       // the queue is a ring: no shifting
                         refine(32);
-                        uint32_t tid4[4];
-                        uint64_t tw4[4];
-                        uint8_t tc4[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {             // qn - 32 <= 128 left to shift
-                            const int q = 32 + lane + 32 * k;
-                            if (q < qn) {
-                                tid4[k] = qid[q];
-                                tw4[k] = qw[q];
-                                tc4[k] = qc[q];
-                            }
-                        }
-                        __syncwarp();
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const int q = 32 + lane + 32 * k;
-                            if (q < qn) {
-                                qid[q - 32] = tid4[k];
-                                qw[q - 32] = tw4[k];
-                                qc[q - 32] = tc4[k];
-                            }
-                        }
+                        qh += 32;
+                        qh -= qh >= kQ ? kQ : 0;
                         qn -= 32;
                         __syncwarp();
                     }
