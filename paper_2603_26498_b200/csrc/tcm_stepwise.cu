@@ -18,6 +18,8 @@
 //   a5  advances the clock, stamps first tokens and runs the decode calendar (same integer
 //       arithmetic as the fused engine), with the decode-only fast-forward (Lemma L3).
 // Nothing here relies on Lemma L1 (class-FIFO order), so any per-request key fits this path.
+#include <cooperative_groups.h>
+
 #include "tcm_k1.cuh"
 #include "tcm_stepwise.cuh"
 
@@ -215,6 +217,14 @@ template <int G>
 __device__ __forceinline__ void group_sync() {
     if (G == 1) __syncwarp();
     else __syncthreads();
+}
+
+// CL > 1: a thread-block cluster of CL CTAs runs one replica (few huge queues); the group's state
+// lives in rank 0's shared memory and the other CTAs reach it through distributed shared memory.
+template <int G, int CL>
+__device__ __forceinline__ void gsync() {
+    if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
+    else group_sync<G>();
 }
 
 // Prologue (warp 0 of the group): ingest, idle jumps, decode-only fast-forward.
@@ -423,7 +433,7 @@ __device__ __noinline__ void sw_preempt(const ModelConst& m, const TraceDev& t, 
 
 // GR: some replica of the trace runs TCM_KV_GROWTH (NEXT-1); the plain instantiation compiles
 // the growth code out of the hot path.
-template <int G, bool GR>
+template <int G, bool GR, int CL>
 __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
                                                       int count_active) {
     constexpr int kGroups = kWarpsPerBlock / G;
@@ -434,8 +444,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
     uint64_t* ring_a = reinterpret_cast<uint64_t*>(dsm);
     uint32_t* ring_s = reinterpret_cast<uint32_t*>(dsm + (size_t)kWarpsPerBlock * kStages * 128 * 8);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int group = warp / G, wg = warp % G;       // warp index inside the group
-    GroupSmem<G>& sm = smg[group];
+    const int group = warp / G, wl = warp % G;       // warp index inside this CTA's group
+    uint32_t crank = 0;
+    if constexpr (CL > 1) crank = cooperative_groups::this_cluster().block_rank();
+    const int wg = (int)crank * G + wl;               // warp index inside the replica's group (all CTAs)
+    GroupSmem<G>& sm = smg[group];                    // this CTA: class pack, per-warp queues and lists
+    GroupSmem<G>& gsm = [&]() -> GroupSmem<G>& {      // the group's state (rank 0 of a cluster)
+        if constexpr (CL > 1) return *cooperative_groups::this_cluster().map_shared_rank(&smg[0], 0);
+        else return smg[group];
+    }();
     if (tid < 16) {
         s_lnR[tid] = kLnR[tid];
         s_lnT[tid] = kLnT[tid];
@@ -444,15 +461,17 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
     __syncthreads();
     const K1Tables tb{s_lnR, s_lnT, s_expT};
 
-    for (uint32_t r = blockIdx.x * kGroups + group; r < t.R; r += gridDim.x * kGroups) {
+    const uint32_t r0 = CL > 1 ? blockIdx.x / CL : blockIdx.x * kGroups + group;
+    const uint32_t rstep = CL > 1 ? gridDim.x / CL : gridDim.x * kGroups;
+    for (uint32_t r = r0; r < t.R; r += rstep) {
       // up to kItersPerLaunch engine iterations of this replica per launch (each one the full
       // a1-a5 step); tcm_step's budget (head[1]) still bounds the total
       for (int kit = 0; kit < kItersPerLaunch; ++kit) {
-        if (wg == 0) sw_prologue<G, GR>(m, t, r, sm, lane);
-        group_sync<G>();
-        if (sm.mode == 0) {
-            if (wg == 0 && lane == 0) t.state[r] = sm.st;
-            group_sync<G>();
+        if (wg == 0) sw_prologue<G, GR>(m, t, r, gsm, lane);
+        gsync<G, CL>();
+        if (gsm.mode == 0) {
+            if (wg == 0 && lane == 0) t.state[r] = gsm.st;
+            gsync<G, CL>();
             break;
         }
 
@@ -468,29 +487,29 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
         const uint8_t* rsc = t.req_state + base;
         uint8_t* rs = t.req_state + base;
         uint32_t* rem = remv + base;
-        const uint64_t clock = sm.st.clock;
+        const uint64_t clock = gsm.st.clock;
         const bool growth = GR && (prm.flags & TCM_KV_GROWTH) != 0;
-        if (wg == 0) {
-            {   // stage the replica's ClassPack (144 B) in shared memory
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(t.kpack + r);
-                uint32_t* dst = reinterpret_cast<uint32_t*>(&sm.kp);
-                for (int q = lane; q < (int)(sizeof(ClassPack) / 4); q += 32) dst[q] = src[q];
-            }
+        if (wl == 0) {   // stage the replica's ClassPack (144 B) in this CTA's shared memory
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(t.kpack + r);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(&sm.kp);
+            for (int q = lane; q < (int)(sizeof(ClassPack) / 4); q += 32) dst[q] = src[q];
             __syncwarp();
-            if (growth) sw_preempt(m, t, r, base, rs, rem, prio, tb, sm.kp, sm.st, lane);
+        }
+        if (wg == 0) {
+            if (growth) sw_preempt(m, t, r, base, rs, rem, prio, tb, sm.kp, gsm.st, lane);
             if (lane == 0) {
                 const uint32_t B = prm.chunk_budget;
-                sm.left = B > sm.st.n_dec ? B - sm.st.n_dec : 0;     // R8
-                sm.tok = 0;
-                sm.inl = 0;
-                sm.blocked = 0;
-                sm.has_th = 0;
-                sm.npart = 0;
-                sm.ndone = 0;
+                gsm.left = B > gsm.st.n_dec ? B - gsm.st.n_dec : 0;     // R8
+                gsm.tok = 0;
+                gsm.inl = 0;
+                gsm.blocked = 0;
+                gsm.has_th = 0;
+                gsm.npart = 0;
+                gsm.ndone = 0;
             }
         }
-        group_sync<G>();
-        const uint32_t lo = sm.st.head[0], hi = sm.st.nxt;     // after any preemption (NEXT-1)
+        gsync<G, CL>();
+        const uint32_t lo = gsm.st.head[0], hi = gsm.st.nxt;     // after any preemption (NEXT-1)
         const bool filter_ok = sm.kp.filter_ok != 0;
         // compound sort keys need every key in [1e-12, 2^17): P <= Smax_c
         const bool cmp_ok = prio && sm.kp.Smax[0] < 65536.0 && sm.kp.Smax[1] < 65536.0 && sm.kp.Smax[2] < 65536.0;
@@ -498,9 +517,9 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
 
         for (int pass = 0;; ++pass) {
             const bool first_pass = pass == 0;
-            const bool has_th = sm.has_th;
-            const uint64_t thk = sm.thk;
-            const uint32_t thi = sm.thi;
+            const bool has_th = gsm.has_th;
+            const uint64_t thk = gsm.thk;
+            const uint32_t thi = gsm.thi;
             const double Pth = __longlong_as_double((long long)thk);
             // ---- a2 + a3: stream the window; every pending request gets an FP32 bound on its
             // priority; those that could still enter this warp's exact top-32 (or hold KV as a
@@ -566,9 +585,9 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
             };
             int qn = 0, qh = 0;                      // refine queue: count and ring head
             constexpr int kQ = GroupSmem<G>::kQ;
-            uint32_t* qid = sm.qid[wg];
-            uint64_t* qw = sm.qw[wg];
-            uint8_t* qc = sm.qc[wg];
+            uint32_t* qid = sm.qid[wl];
+            uint64_t* qw = sm.qw[wl];
+            uint8_t* qc = sm.qc[wl];
             auto take = [&](uint64_t key, uint32_t id, bool enter) {   // warp-collective
                 const uint32_t em = __ballot_sync(0xFFFFFFFFu, enter);
                 if (em == 0) return;
@@ -658,10 +677,10 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                     const int c = cc & RS_CLS;
                     key = prio ? k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qwl, tb) : 0;
                     if (first_pass && (cc & RS_RES)) {                 // partial: remember its key
-                        const int slot = atomicAdd(&sm.npart, 1);
+                        const int slot = atomicAdd(&gsm.npart, 1);
                         if (slot < kMaxPart) {
-                            sm.part[slot] = id;
-                            sm.partkey[slot] = key;
+                            gsm.part[slot] = id;
+                            gsm.partkey[slot] = key;
                         }
                     }
                     const bool valid = !(has_th && !before(thk, thi, key, id));
@@ -670,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 take(key, id, enter);
             };
             const int64_t gstart = (int64_t)((base + lo) & ~3ull) - (int64_t)base;   // 4-aligned globally
-            const int64_t stride = (int64_t)G * 128;
+            const int64_t stride = (int64_t)G * CL * 128;
             // cp.async ring: kStages chunks of 128 requests per warp in flight; lane l copies and
             // later consumes exactly its own 4 requests (32 B of arrivals + 4 state bytes), so
             // no cross-lane barrier is needed, only cp.async.wait_group.
@@ -736,10 +755,10 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                         any_direct |= valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
                                       before(key, (uint32_t)e, kk, ki);
                         if (valid && first_pass && (sb & RS_RES)) {
-                            const int slot = atomicAdd(&sm.npart, 1);
+                            const int slot = atomicAdd(&gsm.npart, 1);
                             if (slot < kMaxPart) {
-                                sm.part[slot] = (uint32_t)e;
-                                sm.partkey[slot] = key;
+                                gsm.part[slot] = (uint32_t)e;
+                                gsm.partkey[slot] = key;
                             }
                         }
                     } else {
@@ -791,22 +810,39 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
             cp_async_wait<0>();
             if (qn > 0) refine(qn);
             if (G > 1) {
-                sm.wkey[wg][lane] = lk;
-                sm.wid[wg][lane] = li;
+                sm.wkey[wl][lane] = lk;
+                sm.wid[wl][lane] = li;
             }
-            group_sync<G>();
+            gsync<G, CL>();
+            if constexpr (CL > 1) {
+                // each CTA's warp 0 merges its warps' lists, then rank 0 merges the CTA lists (DSMEM)
+                if (wl == 0) {
+#pragma unroll 1
+                    for (int w = 1; w < G; ++w) warp_merge(lk, li, sm.wkey[w][lane], sm.wid[w][lane], lane);
+                    sm.wkey[0][lane] = lk;
+                    sm.wid[0][lane] = li;
+                }
+                gsync<G, CL>();
+                if (wg == 0) {
+#pragma unroll 1
+                    for (int q = 1; q < CL; ++q) {
+                        const GroupSmem<G>* rmt = cooperative_groups::this_cluster().map_shared_rank(&smg[0], q);
+                        warp_merge(lk, li, rmt->wkey[0][lane], rmt->wid[0][lane], lane);
+                    }
+                }
+            }
 
             // ---- a4: warp 0 of the group merges the lists and prefix-scans the admission
             if (wg == 0) {
-                if (G > 1) {
+                if (G > 1 && CL == 1) {
 #pragma unroll 1
                     for (int w = 1; w < G; ++w) warp_merge(lk, li, sm.wkey[w][lane], sm.wid[w][lane], lane);
                 }
                 const bool valid = li != NIL;
                 const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-                const uint64_t left = sm.left;
-                const uint64_t kv = sm.st.kv_free;
-                const bool blocked_prev = sm.blocked;
+                const uint64_t left = gsm.left;
+                const uint64_t kv = gsm.st.kv_free;
+                const bool blocked_prev = gsm.blocked;
                 uint32_t f = 0, rr = 0, il = 0;
                 bool res = false, prev = false;
                 if (valid) {
@@ -845,7 +881,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 const uint32_t adm_mask = __ballot_sync(0xFFFFFFFFu, admitted && !prev);   // first admissions
                 const uint32_t rank = __popc(adm_mask & ((1u << lane) - 1));
                 if (admitted) {
-                    if (!prev) t.admit_seq[base + li] = sm.st.seq + rank;
+                    if (!prev) t.admit_seq[base + li] = gsm.st.seq + rank;
                     rs[li] = (uint8_t)(rsc[li] | RS_RES | (growth ? RS_PREV : 0));
                     if (growth) {
                         t.kvres[base + li] = f;
@@ -857,8 +893,8 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                     rem[li] = nr;
                     if (nr == 0) {
                         rs[li] = (uint8_t)(rs[li] | RS_FT);
-                        const int d = atomicAdd(&sm.ndone, 1);
-                        if (d < kMaxDone) sm.done[d] = li;
+                        const int d = atomicAdd(&gsm.ndone, 1);
+                        if (d < kMaxDone) gsm.done[d] = li;
                     }
                 }
                 const uint64_t sum_chunk = warp_sum64(chunk);
@@ -869,33 +905,33 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 const uint64_t lastk = __shfl_sync(0xFFFFFFFFu, lk, lastl);
                 const uint32_t lasti = __shfl_sync(0xFFFFFFFFu, li, lastl);
                 if (lane == 0) {
-                    sm.st.seq += __popc(adm_mask);
-                    sm.st.kv_free = kv - sum_f;
-                    sm.left = left - sum_chunk;
-                    sm.tok += sum_chunk;
-                    sm.inl += sum_inl;
-                    if (any_misfit) sm.blocked = 1;
+                    gsm.st.seq += __popc(adm_mask);
+                    gsm.st.kv_free = kv - sum_f;
+                    gsm.left = left - sum_chunk;
+                    gsm.tok += sum_chunk;
+                    gsm.inl += sum_inl;
+                    if (any_misfit) gsm.blocked = 1;
                     if (nvalid > 0) {
-                        sm.thk = lastk;
-                        sm.thi = lasti;
-                        sm.has_th = 1;
+                        gsm.thk = lastk;
+                        gsm.thi = lasti;
+                        gsm.has_th = 1;
                     }
                     // 1: budget left, nothing blocked, batch full -> next 32 candidates;
                     // 2: budget left but new admissions blocked (R6) -> only partials ranked
                     //    below this batch can still receive chunks.
-                    sm.pass_more = 0;
-                    if (sm.left > 0) sm.pass_more = sm.blocked ? 2 : (nvalid == kTop ? 1 : 0);
-                    if (sm.npart > kMaxPart) sm.st.status = ST_PARTIAL_OVERFLOW;
+                    gsm.pass_more = 0;
+                    if (gsm.left > 0) gsm.pass_more = gsm.blocked ? 2 : (nvalid == kTop ? 1 : 0);
+                    if (gsm.npart > kMaxPart) gsm.st.status = ST_PARTIAL_OVERFLOW;
                 }
                 __syncwarp();
-                if (sm.pass_more == 2) {
-                    const int np = sm.npart < kMaxPart ? sm.npart : kMaxPart;
+                if (gsm.pass_more == 2) {
+                    const int np = gsm.npart < kMaxPart ? gsm.npart : kMaxPart;
                     uint64_t pk = 0;
                     uint32_t pi = NIL;
                     if (lane < np) {
-                        pk = sm.partkey[lane];
-                        pi = sm.part[lane];
-                        if (sm.has_th && !before(sm.thk, sm.thi, pk, pi)) {   // already scanned
+                        pk = gsm.partkey[lane];
+                        pi = gsm.part[lane];
+                        if (gsm.has_th && !before(gsm.thk, gsm.thi, pk, pi)) {   // already scanned
                             pk = 0;
                             pi = NIL;
                         }
@@ -904,36 +940,36 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                     for (int q = 0; q < np; ++q) {                        // <= 3 under Lemma L2
                         const uint32_t id = __shfl_sync(0xFFFFFFFFu, pi, q);
                         if (id == NIL) break;
-                        if (lane == 0 && sm.left > 0) {
+                        if (lane == 0 && gsm.left > 0) {
                             const uint32_t rr2 = rem[id];
-                            const uint64_t ch = rr2 < sm.left ? rr2 : sm.left;
+                            const uint64_t ch = rr2 < gsm.left ? rr2 : gsm.left;
                             rem[id] = rr2 - (uint32_t)ch;
-                            sm.left -= ch;
-                            sm.tok += ch;
+                            gsm.left -= ch;
+                            gsm.tok += ch;
                             if (rr2 == ch) {
                                 rs[id] = (uint8_t)(rs[id] | RS_FT);
-                                const int d = sm.ndone++;
-                                if (d < kMaxDone) sm.done[d] = id;
+                                const int d = gsm.ndone++;
+                                if (d < kMaxDone) gsm.done[d] = id;
                             }
                         }
                         __syncwarp();
                     }
-                    if (lane == 0) sm.pass_more = 0;
+                    if (lane == 0) gsm.pass_more = 0;
                 }
             }
-            group_sync<G>();
-            if (sm.pass_more != 1) break;
+            gsync<G, CL>();
+            if (gsm.pass_more != 1) break;
         }
 
         // ---- a5: clock, calendar, first tokens (warp 0 of the group)
         if (wg == 0) {
-            ReplicaState& st = sm.st;
+            ReplicaState& st = gsm.st;
             if (lane == 0) {
-                if (sm.tok == 0 && st.n_dec == 0) {
+                if (gsm.tok == 0 && st.n_dec == 0) {
                     st.status = ST_DEADLOCK;
                     st.flags |= FLAG_FINISHED;
                 }
-                st.clock += m.c0 + m.cp * sm.tok + m.cd * (uint64_t)st.n_dec + sm.inl;
+                st.clock += m.c0 + m.cp * gsm.tok + m.cd * (uint64_t)st.n_dec + gsm.inl;
                 st.iter++;
                 st.head[1]--;
                 st.decisions++;
@@ -947,7 +983,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
             __syncwarp();
             const uint64_t now = st.clock;
             const uint64_t it = st.iter;
-            const int nd = sm.ndone;
+            const int nd = gsm.ndone;
             const uint16_t* out = t.out + base;
             uint32_t* cal = t.cal + (size_t)r * kCalSlots;
             uint32_t* occ = t.occ + (size_t)r * kCalWords;
@@ -992,7 +1028,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 }
             };
             if (nd <= kMaxDone) {
-                for (int q = lane; q < nd; q += 32) stamp(sm.done[q]);
+                for (int q = lane; q < nd; q += 32) stamp(gsm.done[q]);
             } else {
                 for (uint32_t i = lo + lane; i < hi; i += 32)
                     if (rs[i] & RS_FT) stamp(i);
@@ -1022,11 +1058,12 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 t.state[r] = st;
             }
         }
-        group_sync<G>();
+        gsync<G, CL>();
       }
-        if (wg == 0 && lane == 0 && count_active && !(sm.st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
-        group_sync<G>();
+        if (wg == 0 && lane == 0 && count_active && !(gsm.st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
+        gsync<G, CL>();
     }
+    if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
 }
 
 // ReplicaState.head[0] = window start lo (oldest possibly-pending id), head[1] = remaining
@@ -1065,26 +1102,36 @@ StepwiseWorkspace stepwise_bind(void* p, uint32_t R) {
 namespace {
 struct Launch {
     int grid;
-    int group;   // warps per replica
+    int group;   // warps per replica (per CTA of the cluster)
+    int cluster; // CTAs per replica (thread-block cluster; 1 = none)
 };
+constexpr int kCluster = 8;    // CTAs per replica for a few huge queues (portable cluster size)
 
 Launch stepwise_config(uint32_t R) {
     int dev = 0, sms = 148, per_sm1 = 1, per_sm8 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_step<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1, false>, kThreads, kRingBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8, false>, kThreads, kRingBytes);
+    cudaFuncSetAttribute(k_step<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<8, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<1, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<8, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<8, false, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaFuncSetAttribute(k_step<8, true, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1, false, 1>, kThreads, kRingBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8, false, 1>, kThreads, kRingBytes);
     if (per_sm1 < 1) per_sm1 = 1;
     if (per_sm8 < 1) per_sm8 = 1;
     // Warp per replica when there are enough replicas to fill every warp slot twice over;
     // otherwise a CTA per replica so that few (large) queues still stream at full width.
     const uint64_t warp_slots = (uint64_t)sms * per_sm1 * kWarpsPerBlock;
     Launch l;
-    if ((uint64_t)R >= 2 * warp_slots) {
+    l.cluster = 1;
+    if ((uint64_t)R * kCluster * 2 <= (uint64_t)sms) {
+        // few queues: a cluster of kCluster CTAs streams each one (DSMEM merge), 64 warps per queue
+        l.group = 8;
+        l.cluster = kCluster;
+        l.grid = (int)R * kCluster;
+    } else if ((uint64_t)R >= 2 * warp_slots) {
         l.group = 1;
         const uint64_t need = ((uint64_t)R + kWarpsPerBlock - 1) / kWarpsPerBlock;
         const uint64_t cap = (uint64_t)sms * per_sm1;
@@ -1117,12 +1164,29 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         if (cudaEventRecord(ev_begin, s) != cudaSuccess) return TCM_E_CUDA;
         for (uint32_t q = 0; q < this_chunk; ++q) {
             const int last = q + 1 == this_chunk;
-            if (t.any_growth) {
-                if (L.group == 1) k_step<1, true><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
-                else k_step<8, true><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+            if (L.cluster > 1) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(L.grid);
+                cfg.blockDim = dim3(kThreads);
+                cfg.dynamicSmemBytes = kRingBytes;
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = L.cluster;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                cudaError_t e = t.any_growth
+                    ? cudaLaunchKernelEx(&cfg, k_step<8, true, kCluster>, m, t, remv, d_active, last)
+                    : cudaLaunchKernelEx(&cfg, k_step<8, false, kCluster>, m, t, remv, d_active, last);
+                if (e != cudaSuccess) return TCM_E_CUDA;
+            } else if (t.any_growth) {
+                if (L.group == 1) k_step<1, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+                else k_step<8, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
             } else {
-                if (L.group == 1) k_step<1, false><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
-                else k_step<8, false><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+                if (L.group == 1) k_step<1, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+                else k_step<8, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
             }
             (*launches)++;
         }
