@@ -83,3 +83,23 @@ def test_allreduce_equals_single_process():
     H, C = aggregate_shard(small_c4(0, 1))
     np.testing.assert_array_equal(h, H)
     np.testing.assert_array_equal(c, C)
+
+
+def test_c5_and_growth_sweeps_shard_cleanly():
+    # C5 (1M replicas at 8 GPUs): rank r holds seeds r, r+8, ... of every one of the 16,384 cells;
+    # shards are disjoint and together equal the single-process sweep (checked at 1/64 scale)
+    nc = len(W.c5_cells())
+    assert nc == 16 * 8 * 16 * 8
+    full = set(W.rank_ids(nc, 16, 0, 1))
+    parts = [set(W.rank_ids(nc, 16, r, 8)) for r in range(8)]
+    assert sum(len(p) for p in parts) == len(full) and set().union(*parts) == full
+    for r, p in enumerate(parts):
+        assert {g % nc for g in p} == set(range(nc)) and all((g // nc) % 8 == r for g in p)
+    # NEXT-1 sweep: every replica has the growth flag and footprint + out - 1 fits its KV (R28)
+    sw = W.c4_growth(0, 1, replicas_per_gpu=64, n_requests=200)
+    assert np.all(sw.params["flags"] == 2)
+    tr = T.generate(sw.gen)
+    for r in range(sw.n_replicas):
+        a, b = int(tr.offset[r]), int(tr.offset[r + 1])
+        kv = int(sw.params["kv_capacity"][r])
+        assert np.all(tr.footprint[a:b].astype(np.int64) + tr.out_tokens[a:b] - 1 <= kv)
