@@ -193,6 +193,12 @@ def run_tcm(args, rank, world, local):
     if args.workload == "c5":
         # C5 (BASELINE.json configs[4]): 1M replicas on 8 GPUs = 131,072 per GPU (weak scaling)
         sw = W.c5(rank, world, replicas=args.replicas * world, n_requests=args.requests)
+    elif args.workload == "c3":
+        # C3 (configs[2]): 4,096 replicas x 10k, lambda x alpha sweep, per GPU
+        sw = W.c3(rank, world, replicas=args.replicas * world, n_requests=args.requests)
+    elif args.workload == "c1":
+        # C1 (configs[0]): one replica x 1,000 requests (TCM), a single serial engine per GPU
+        sw = W.c1()
     else:
         sw = W.c4(rank, world, replicas_per_gpu=args.replicas, n_requests=args.requests)
     R, N = sw.n_replicas, sw.n_requests
@@ -279,7 +285,12 @@ def run_tcm(args, rank, world, local):
         except Exception:
             traffic = None
 
-    if args.workload == "c5":
+    if args.workload == "c3":
+        wl = (f"C3 sweep: {R} replicas x {args.requests} requests per GPU (16 lambda x 16 alpha x seeds, 70/25/5, "
+              "TCM), fused engine")
+    elif args.workload == "c1":
+        wl = "C1: 1 replica x 1,000 requests (70/25/5, 2 req/s, TCM), fused engine: one serial engine, latency-bound"
+    elif args.workload == "c5":
         wl = (f"C5 full policy sweep: {R} replicas x {args.requests} requests per GPU (16 lambda x 8 mixes x 16 alpha x "
               f"8 chunk budgets = {sw.n_cells} cells x seeds; 1M replicas at 8 GPUs), fused engine, per-request results "
               "kept in the library workspace")
@@ -576,7 +587,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["tcm", "reference"], default="tcm")
-    ap.add_argument("--workload", choices=["c4", "c5"], default="c4")
+    ap.add_argument("--workload", choices=["c4", "c5", "c3", "c1"], default="c4")
     ap.add_argument("--replicas", type=int, default=None, help="replicas per GPU (C4 65,536; C5 131,072)")
     ap.add_argument("--requests", type=int, default=10_000)
     ap.add_argument("--ref-requests", type=int, default=2000, help="oracle sample: requests per replica")
@@ -592,9 +603,11 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     if args.replicas is None:
-        args.replicas = 131072 if args.workload == "c5" else 65536
-    if args.workload == "c5":
-        # the C5 step moves 51 GB of per-request data; its e2e leg and the C4-specific legs are not run
+        args.replicas = {"c5": 131072, "c3": 4096, "c1": 1}.get(args.workload, 65536)
+    if args.workload == "c1":
+        args.requests = 1000
+    if args.workload != "c4":
+        # the C4-specific legs (e2e, stepwise C2', NEXT-1) run with the default workload only
         args.skip_e2e = args.skip_step = args.skip_next1 = True
     rank, world, local = dist_init(args)
     if args.impl == "reference":
