@@ -249,13 +249,17 @@ __global__ void k_fpack(ModelConst m, TraceDev t) {
     }
 }
 
+// lpw: replicas per warp (a power of two <= 32).  With fewer replicas than resident lanes the warps
+// carry fewer replicas each, so a warp pays for the union of fewer divergent paths.
 __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t, uint32_t max_iters,
-                                                    uint32_t* active) {
+                                                    uint32_t* active, uint32_t lpw) {
     __shared__ uint32_t occ_s[kCalWords][kThreads];
     // work counters live in shared memory during the loop (registers are the scarce resource)
     __shared__ unsigned long long s_dec[kThreads], s_sum[kThreads], s_ff[kThreads];
     __shared__ uint32_t s_idle[kThreads], s_maxp[kThreads], s_scan[kThreads];
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t gthread = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((gthread & 31) >= lpw) return;
+    const uint32_t r = (gthread >> 5) * lpw + (gthread & 31);
     if (r >= t.R) return;
     ReplicaState st = t.state[r];
     if (st.flags & FLAG_FINISHED) return;
@@ -793,8 +797,18 @@ void launch_fused_prologue(const ModelConst& m, const TraceDev& t, cudaStream_t 
 
 void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, uint32_t* d_active,
                   cudaStream_t s) {
-    const uint32_t blocks = (t.R + kThreads - 1) / kThreads;
-    k_fused<<<blocks, kThreads, 0, s>>>(m, t, max_iters, d_active);
+    // replicas per warp: the smallest power of two that keeps every replica in the resident warps
+    int dev = 0, sms = 148, per_sm = 8;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused, kThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t warps = (uint64_t)sms * per_sm * (kThreads / 32);
+    uint32_t lpw = 1;
+    while (lpw < 32 && (uint64_t)lpw * warps < t.R) lpw <<= 1;
+    const uint64_t nwarps = ((uint64_t)t.R + lpw - 1) / lpw;
+    const uint32_t blocks = (uint32_t)((nwarps * 32 + kThreads - 1) / kThreads);
+    k_fused<<<blocks, kThreads, 0, s>>>(m, t, max_iters, d_active, lpw);
 }
 
 void launch_fused_stamp(const TraceDev& t, cudaStream_t s) {
