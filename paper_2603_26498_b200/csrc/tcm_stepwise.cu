@@ -19,6 +19,7 @@
 //       arithmetic as the fused engine), with the decode-only fast-forward (Lemma L3).
 // Nothing here relies on Lemma L1 (class-FIFO order), so any per-request key fits this path.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "tcm_k1.cuh"
 #include "tcm_stepwise.cuh"
@@ -1107,7 +1108,7 @@ struct Launch {
 };
 constexpr int kCluster = 8;    // CTAs per replica for a few huge queues (portable cluster size)
 
-Launch stepwise_config(uint32_t R) {
+Launch stepwise_config(uint32_t R, uint64_t N) {
     int dev = 0, sms = 148, per_sm1 = 1, per_sm8 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1121,17 +1122,28 @@ Launch stepwise_config(uint32_t R) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8, false, 1>, kThreads, kRingBytes);
     if (per_sm1 < 1) per_sm1 = 1;
     if (per_sm8 < 1) per_sm8 = 1;
-    // Warp per replica when there are enough replicas to fill every warp slot twice over;
-    // otherwise a CTA per replica so that few (large) queues still stream at full width.
+    // Warp per replica unless the queues are few and huge: a CTA per replica only when there are
+    // fewer replicas than twice the warp slots AND they average >= 8,192 requests (measured: for
+    // sweeps of ~1k-request replicas a warp per replica is 2.2x faster, its iterations need no
+    // block barriers), and a cluster for a handful of queues.
     const uint64_t warp_slots = (uint64_t)sms * per_sm1 * kWarpsPerBlock;
     Launch l;
     l.cluster = 1;
-    if ((uint64_t)R * kCluster * 2 <= (uint64_t)sms) {
+    const char* force = getenv("TCM_SW_GROUP");        // development A/B knob: "1", "8" or "cluster"
+    const int fg = force ? (force[0] == 'c' ? 64 : atoi(force)) : 0;
+    if (fg == 1 || fg == 8) {
+        l.group = fg;
+        const uint64_t cap = (uint64_t)sms * (fg == 1 ? per_sm1 : per_sm8);
+        const uint64_t need = fg == 1 ? ((uint64_t)R + kWarpsPerBlock - 1) / kWarpsPerBlock : (uint64_t)R;
+        l.grid = (int)(need < cap ? need : cap);
+        return l;
+    }
+    if (fg == 64 || (uint64_t)R * kCluster * 2 <= (uint64_t)sms) {
         // few queues: a cluster of kCluster CTAs streams each one (DSMEM merge), 64 warps per queue
         l.group = 8;
         l.cluster = kCluster;
         l.grid = (int)R * kCluster;
-    } else if ((uint64_t)R >= 2 * warp_slots) {
+    } else if ((uint64_t)R >= 2 * warp_slots || N < (uint64_t)R * 8192) {
         l.group = 1;
         const uint64_t need = ((uint64_t)R + kWarpsPerBlock - 1) / kWarpsPerBlock;
         const uint64_t cap = (uint64_t)sms * per_sm1;
@@ -1149,7 +1161,7 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
                         uint32_t* d_active, cudaStream_t s, uint64_t* launches, cudaEvent_t ev_begin,
                         cudaEvent_t ev_end, double* kernel_ms) {
     uint32_t* remv = reinterpret_cast<uint32_t*>(w.base);
-    const Launch L = stepwise_config(t.R);
+    const Launch L = stepwise_config(t.R, t.N);
     k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, max_iters);
     (*launches)++;
     // Each k_step launch advances every active replica by one iteration (or one fast-forward);

@@ -167,3 +167,12 @@ def test_growth_edge_cases():
         c = check(tr, params, out, range(len(reqs)))
         assert st["requests_done"] == tr.n_requests
         assert c["preemptions"] > 0 and st["preemptions"] == c["preemptions"]
+
+
+@pytest.mark.parametrize("mode", ["1", "8", "cluster"])
+def test_growth_launch_modes_bit_exact(mode, monkeypatch):
+    monkeypatch.setenv("TCM_SW_GROUP", mode)
+    tr, params = growth_sweep(24, 400, 75)
+    out, st = run_gpu(tr, params)
+    c = check(tr, params, out, range(24))
+    assert c["preemptions"] > 0 and st["preemptions"] == c["preemptions"]

@@ -303,3 +303,14 @@ def test_calibrated_thresholds_bit_exact():
         cfg = tcm.config(engine=engine, thresholds=thr)
         _, out, _ = run_gpu(tr, params, engine, cfg=cfg)
         check_replicas(tr, params, out, range(64), m=m)
+
+
+@pytest.mark.parametrize("mode", ["1", "8", "cluster"])
+def test_stepwise_launch_modes_bit_exact(mode, monkeypatch):
+    # every group mode of k_step (warp, CTA, 8-CTA cluster per replica) on the same sweep; the
+    # automatic choice depends on the replica count and size, so force each one (TCM_SW_GROUP)
+    monkeypatch.setenv("TCM_SW_GROUP", mode)
+    tr, params = sweep(40, 400, 81)
+    _, out, st = run_gpu(tr, params, tcm.ENGINE_STEPWISE)
+    assert st["requests_done"] == tr.n_requests
+    check_replicas(tr, params, out, range(40))
