@@ -343,7 +343,7 @@ def run_tcm(args, rank, world, local):
         del host
     log("e2e done")
 
-    if rank == 0 and not args.skip_cpu:
+    if rank == 0 and world == 1 and not args.skip_cpu:      # the oracle baseline: rank 0 at N=1 only
         sel = None if sw.n_cells <= 64 else list(range(0, sw.n_cells, sw.n_cells // 32))   # C5: 32 spread cells
         s = oracle_sample(sw, n_trunc=args.ref_requests, cells_sel=sel)
         out["cpu_baseline"] = {"value": s["requests"] / s["wall_s"], "unit": "requests/s", "cores": s["cores"],

@@ -8,6 +8,8 @@
 * C2: one queue with 100k pending requests: the first iterations of both engines vs the oracle
   (max_iters), which re-sorts all 100k keys every iteration.
 * C2': 65,536 replicas x 1,024 pending, one paper-literal step on both engines vs the oracle.
+* C5: rank 0's shard of the 1M-replica sweep (131,072 x 10,000) as `bench.py --workload c5` runs it.
+* NEXT-1: the C4-growth sweep at the size bench.py times (stepwise engine), one replica per cell.
 """
 import multiprocessing as mp
 import os
@@ -155,3 +157,60 @@ def test_c2prime_one_step_both_engines_and_oracle():
         o = O.simulate_trace(tr, r, policy=O.TCM, max_iters=iters)
         np.testing.assert_array_equal(outs[1]["admit_seq"][a:b], o.admit_seq)
         np.testing.assert_array_equal(outs[1]["first_token_us"][a:b], o.first_token_us)
+
+
+def test_c5_per_gpu_shard_sampled_bit_exact():
+    # C5 (configs[4]) at full size per GPU: rank 0's shard of the 1M-replica sweep (131,072
+    # replicas x 10,000 requests), as `bench.py --workload c5` runs it; light sampled cells
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    sw = W.c5(0, 8, replicas=1 << 20, n_requests=10_000)
+    assert sw.n_replicas == 131072
+    sim, dev, res = run_sweep(sw)
+    sim.run()
+    st = sim.stats()
+    assert st["requests_done"] == sw.n_requests and st["first_bad_replica"] == -1
+    cells = sw.params["cell_id"]
+    light = [c for c, cell in enumerate(sw.cells) if cell["rate"] <= 0.5 and cell["budget"] >= 2048][::97][:12]
+    idx = [int(np.nonzero(cells == c)[0][0]) for c in light]
+    compare(sw, res, idx, oracle_many(sw, idx))
+    sim.close()
+    del dev, res
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def _oracle_growth_job(job):
+    gen, pol, kv, alpha, budget = job
+    tr = T.generate(np.array([gen], dtype=T.TG_REPLICA_DTYPE))
+    r = O.simulate_trace_growth(tr, 0, policy=pol, alpha=alpha, kv_capacity=kv, chunk_budget=budget)
+    return r.status, r.admit_seq, r.first_token_us, r.done_us, r.preempt_count, r.preempted_us
+
+
+def test_c4_growth_bench_config_sampled_bit_exact():
+    # NEXT-1 at the size bench.py times (C4-growth, 1,024 x 1,000, stepwise engine): one replica per cell
+    sw = W.c4_growth(0, 1, replicas_per_gpu=1024, n_requests=1000)
+    dev = tcm.generate_device(sw.gen)
+    dev["params"] = torch.from_numpy(sw.params.view(np.uint8)).cuda()
+    res = tcm.alloc_results(sw.n_requests, preemption=True)
+    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE, n_cells=sw.n_cells))
+    sim.load(dev, res)
+    sim.run()
+    st = sim.stats()
+    assert st["requests_done"] == sw.n_requests and st["preemptions"] > 0
+    cells = sw.params["cell_id"]
+    idx = [int(np.nonzero(cells == c)[0][3]) for c in range(sw.n_cells)]
+    jobs = [(sw.gen[i], int(sw.params[i]["policy"]), int(sw.params[i]["kv_capacity"]),
+             float(sw.params[i]["aging_alpha"]), int(sw.params[i]["chunk_budget"])) for i in idx]
+    with mp.get_context("spawn").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+        orc = pool.map(_oracle_growth_job, jobs, chunksize=1)
+    off = np.zeros(sw.n_replicas + 1, np.int64)
+    np.cumsum(sw.gen["n_requests"].astype(np.int64), out=off[1:])
+    for i, (s_, seq, ft, dn, pc, pt) in zip(idx, orc):
+        assert s_ == 0
+        a, b = int(off[i]), int(off[i + 1])
+        for k, v in (("admit_seq", seq), ("first_token_us", ft), ("done_us", dn), ("preempt_count", pc),
+                     ("preempted_us", pt)):
+            np.testing.assert_array_equal(res[k][a:b].cpu().numpy(), v, err_msg=f"replica {i} {k}")
+    sim.close()
