@@ -22,6 +22,8 @@
 // shared memory and a 64-bit word summary in a register.  Finish times are stamped after the
 // launch by k_fstamp from a per-replica log of (iteration, clock) events, and so are first-token
 // times: the loop itself never revisits a request once its prefill is complete.
+#include <cstdlib>
+
 #include "tcm_internal.cuh"
 #include "tcm_k1.cuh"
 
@@ -806,6 +808,10 @@ void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, ui
     const uint64_t warps = (uint64_t)sms * per_sm * (kThreads / 32);
     uint32_t lpw = 1;
     while (lpw < 32 && (uint64_t)lpw * warps < t.R) lpw <<= 1;
+    if (const char* f = getenv("TCM_FUSED_LPW")) {          // development A/B knob
+        const int v = atoi(f);
+        if (v >= 1 && v <= 32) lpw = (uint32_t)v;
+    }
     const uint64_t nwarps = ((uint64_t)t.R + lpw - 1) / lpw;
     const uint32_t blocks = (uint32_t)((nwarps * 32 + kThreads - 1) / kThreads);
     k_fused<<<blocks, kThreads, 0, s>>>(m, t, max_iters, d_active, lpw);
