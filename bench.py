@@ -470,18 +470,21 @@ def bench_next1(args, dev, stream):
         times.append(e0.elapsed_time(e1))
     st = sim.stats()
     ms = times[-1]
-    # per-policy victim classes (R13 smart thresholds: text < 4096 tokens is a motorcycle)
+    # per policy and class (R13 smart thresholds): fig:preemptions
+    from paper_2603_26498_b200 import metrics as M
     pc = res["preempt_count"].cpu().numpy()
-    fp = tr["footprint"].cpu().numpy().view(np.uint32)
+    pt = res["preempted_us"].cpu().numpy()
+    fp = tr["footprint"].cpu().numpy()
     md = tr["modality"].cpu().numpy()
     off = tr["req_offset"].cpu().numpy().astype(np.int64)
     pol = np.repeat(sw.params["policy"], np.diff(off))
-    moto = (md == 0) & (fp < 4096)
     by = {}
     for name, p in (("FCFS", tcm.POLICY_FCFS), ("TCM", tcm.POLICY_TCM)):
         sel = pol == p
-        by[name] = {"preemptions": int(pc[sel].sum()), "motorcycle_preemptions": int(pc[sel & moto].sum()),
-                    "requests_preempted": int((pc[sel] > 0).sum())}
+        summ = M.preemption_summary(md[sel], fp[sel], pc[sel], pt[sel])
+        by[name] = {"preemptions": summ["all"]["preemptions"], "motorcycle_preemptions": summ["M"]["preemptions"],
+                    "requests_preempted": summ["all"]["requests_preempted"],
+                    "preempted_s": {g: round(summ[g]["preempted_s"], 3) for g in ("M", "C", "T")}}
     sim.close()
     return {"workload": f"C4-growth: {sw.n_replicas} replicas x {args.next1_requests} requests (C4 cells, "
                         "KV growth + preemption), stepwise engine",

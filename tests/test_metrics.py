@@ -69,3 +69,19 @@ def test_goodput_binary_search_spec_examples():
     att2 = lambda r: max(0.0, 1.0 - 0.1 * r)
     gs = [M.binary_search_goodput(att2, 0.0, 9.0, th, 0.05) for th in (0.3, 0.5, 0.7, 0.9)]
     assert gs == sorted(gs, reverse=True)
+
+
+def test_preemption_summary_golden_p2():
+    # tests/golden/preemption.json P2: FCFS preempts the text (motorcycle) once for 517,000 us,
+    # TCM preempts the image (car) once for 792,000 us
+    import oracle as O
+    from paper_2603_26498_b200 import metrics as M
+    reqs = dict(arrival_us=[0, 0], footprint=[150, 300], inline_us=[0, 0], out_tokens=[100, 150], modality=[1, 0])
+    f = O.simulate_growth(**reqs, policy=O.FCFS, kv_capacity=460)
+    t = O.simulate_growth(**reqs, policy=O.TCM, kv_capacity=460)
+    sf = M.preemption_summary(reqs["modality"], reqs["footprint"], f.preempt_count, f.preempted_us)
+    st = M.preemption_summary(reqs["modality"], reqs["footprint"], t.preempt_count, t.preempted_us)
+    assert sf["M"] == {"preemptions": 1, "preempted_s": 0.517, "requests_preempted": 1, "requests": 1}
+    assert sf["C"]["preemptions"] == 0 and st["M"]["preemptions"] == 0
+    assert st["C"] == {"preemptions": 1, "preempted_s": 0.792, "requests_preempted": 1, "requests": 1}
+    assert st["all"]["preemptions"] == 1 and st["T"]["requests"] == 0
