@@ -800,12 +800,17 @@ void launch_fused_prologue(const ModelConst& m, const TraceDev& t, cudaStream_t 
 void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, uint32_t* d_active,
                   cudaStream_t s) {
     // replicas per warp: the smallest power of two that keeps every replica in the resident warps
-    int dev = 0, sms = 148, per_sm = 8;
+    static int cached_sms[64] = {}, cached_per_sm[64] = {};    // queried once per device
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused, kThreads, 0);
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t warps = (uint64_t)sms * per_sm * (kThreads / 32);
+    if (cached_sms[dev & 63] == 0) {
+        int sms = 148, per_sm = 8;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused, kThreads, 0);
+        cached_per_sm[dev & 63] = per_sm < 1 ? 1 : per_sm;
+        cached_sms[dev & 63] = sms;
+    }
+    const uint64_t warps = (uint64_t)cached_sms[dev & 63] * cached_per_sm[dev & 63] * (kThreads / 32);
     uint32_t lpw = 1;
     while (lpw < 32 && (uint64_t)lpw * warps < t.R) lpw <<= 1;
     if (const char* f = getenv("TCM_FUSED_LPW")) {          // development A/B knob

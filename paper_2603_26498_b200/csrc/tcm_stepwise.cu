@@ -1108,20 +1108,38 @@ struct Launch {
 };
 constexpr int kCluster = 8;    // CTAs per replica for a few huge queues (portable cluster size)
 
-Launch stepwise_config(uint32_t R, uint64_t N) {
-    int dev = 0, sms = 148, per_sm1 = 1, per_sm8 = 1;
+// Per-device launch facts, queried once (kernel attributes and occupancy do not change).
+struct DevFacts {
+    int sms = 0, per_sm1 = 1, per_sm8 = 1;
+};
+
+DevFacts dev_facts() {
+    static DevFacts cache[64];
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_step<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<8, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<1, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<8, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<8, false, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaFuncSetAttribute(k_step<8, true, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_step<1, false, 1>, kThreads, kRingBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, k_step<8, false, 1>, kThreads, kRingBytes);
-    if (per_sm1 < 1) per_sm1 = 1;
-    if (per_sm8 < 1) per_sm8 = 1;
+    DevFacts& f = cache[dev & 63];
+    if (f.sms == 0) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_step<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+        cudaFuncSetAttribute(k_step<8, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+        cudaFuncSetAttribute(k_step<1, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+        cudaFuncSetAttribute(k_step<8, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+        cudaFuncSetAttribute(k_step<8, false, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+        cudaFuncSetAttribute(k_step<8, true, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+        int p1 = 1, p8 = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_step<1, false, 1>, kThreads, kRingBytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p8, k_step<8, false, 1>, kThreads, kRingBytes);
+        f.per_sm1 = p1 < 1 ? 1 : p1;
+        f.per_sm8 = p8 < 1 ? 1 : p8;
+        f.sms = sms;
+    }
+    return f;
+}
+
+Launch stepwise_config(uint32_t R, uint64_t N) {
+    const DevFacts f = dev_facts();
+    const int sms = f.sms, per_sm1 = f.per_sm1, per_sm8 = f.per_sm8;
     // Warp per replica unless the queues are few and huge: a CTA per replica only when there are
     // fewer replicas than twice the warp slots AND they average >= 8,192 requests (measured: for
     // sweeps of ~1k-request replicas a warp per replica is 2.2x faster, its iterations need no
