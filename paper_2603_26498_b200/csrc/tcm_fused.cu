@@ -771,16 +771,18 @@ __device__ __forceinline__ uint64_t log_clock(const uint64_t* log, uint32_t nlog
     return __ldg(log + 2 * lo + 1);
 }
 
-__global__ void k_fstamp(TraceDev t) {
-    const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t lane = threadIdx.x & 31;
+// wpr warps per replica (1 for sweeps; more for a few huge queues so the stamping is not one warp)
+__global__ void k_fstamp(TraceDev t, uint32_t wpr) {
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t r = gw / wpr;
+    const uint32_t lane = (gw % wpr) * 32 + (threadIdx.x & 31);
     if (r >= t.R) return;
     const uint64_t a = t.offset[r];
     const uint32_t n = (uint32_t)(t.offset[r + 1] - a);
     const uint64_t iter = t.state[r].iter;
     const uint32_t nlog = t.state[r].nlog;
     const uint64_t* log = t.fw.log + 4 * a;
-    for (uint32_t i = lane; i < n; i += 32) {
+    for (uint32_t i = lane; i < n; i += 32 * wpr) {
         const uint64_t ft = t.first_token[a + i];
         if (ft & kPending) t.first_token[a + i] = log_clock(log, nlog, ft & ~kPending);
         const uint64_t F = t.fw.fin[a + i];
@@ -824,8 +826,11 @@ void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, ui
 
 void launch_fused_stamp(const TraceDev& t, cudaStream_t s) {
     const uint32_t threads = 256;
-    const uint64_t blocks = ((uint64_t)t.R * 32 + threads - 1) / threads;
-    k_fstamp<<<(uint32_t)blocks, threads, 0, s>>>(t);
+    const uint64_t avg = t.R ? t.N / t.R : 0;
+    uint32_t wpr = 1;                                   // ~4k requests per warp, <= 4,096 warps in all
+    while (wpr < 64 && (uint64_t)wpr * 4096 < avg && (uint64_t)t.R * wpr * 2 <= 4096) wpr <<= 1;
+    const uint64_t blocks = ((uint64_t)t.R * wpr * 32 + threads - 1) / threads;
+    k_fstamp<<<(uint32_t)blocks, threads, 0, s>>>(t, wpr);
 }
 
 }  // namespace tcm
