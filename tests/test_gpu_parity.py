@@ -314,3 +314,72 @@ def test_stepwise_launch_modes_bit_exact(mode, monkeypatch):
     _, out, st = run_gpu(tr, params, tcm.ENGINE_STEPWISE)
     assert st["requests_done"] == tr.n_requests
     check_replicas(tr, params, out, range(40))
+
+
+# ------------------------------------------------------------------------ brute force
+def _tiny_cases(outs=(1, 3)):
+    """SURVEY.md 8(c) brute force on tiny queues (the grid of tests/test_oracle_engine.py)."""
+    import itertools
+    import random
+    fps = [1, 17, 30]
+    arrivals = [0, 1, 3_200_000, 47_000_000, 90_000_000]
+    one = list(itertools.product(arrivals, fps, [0, 95_000_000], list(outs), [0, 1, 2]))
+    rng = random.Random(9)
+    cases = [[a] for a in one]
+    cases += [sorted([rng.choice(one) for _ in range(k)]) for k in (2, 3, 4) for _ in range(600)]
+    return [[list(r) for r in c] for c in cases]
+
+
+@pytest.mark.parametrize("engine", ENGINES, ids=["fused", "stepwise"])
+def test_brute_force_tiny_queues_as_replicas(engine):
+    # every tiny trace x B in {1,3,8} x {FCFS, TCM} as one replica of a single GPU batch, each
+    # compared bit-exactly with the oracle (thresholds that map the footprints to all classes)
+    thr = ((10, 2**32 - 1), (0, 2**32 - 1), (0, 20))
+    m = O.model(thresholds=thr)
+    cases = _tiny_cases()
+    combos = [(c, B, pol) for c in cases for B in (1, 3, 8) for pol in (tcm.POLICY_FCFS, tcm.POLICY_TCM)]
+    tr = T.concat([T.from_requests(c) for c, _, _ in combos])
+    params = tcm.make_params(len(combos), kv_capacity=40)
+    params["chunk_budget"] = [B for _, B, _ in combos]
+    params["policy"] = [p for _, _, p in combos]
+    cfg = tcm.config(engine=engine, thresholds=thr)
+    _, out, st = run_gpu(tr, params, engine, cfg=cfg)
+    assert st["requests_done"] == tr.n_requests and st["first_bad_replica"] == -1
+    for r, (c, B, pol) in enumerate(combos):
+        a, b = int(tr.offset[r]), int(tr.offset[r + 1])
+        o = O.simulate_trace(tr, r, policy=int(pol), kv_capacity=40, chunk_budget=B, m=m)
+        assert o.status == 0
+        assert out["admit_seq"][a:b].tolist() == o.admit_seq.tolist(), (c, B, pol)
+        assert out["first_token_us"][a:b].tolist() == o.first_token_us.tolist(), (c, B, pol)
+        assert out["done_us"][a:b].tolist() == o.done_us.tolist(), (c, B, pol)
+
+
+def test_brute_force_tiny_queues_growth_stepwise():
+    # the same batch under NEXT-1 (KV growth + preemption, R28-R32) on the stepwise engine
+    thr = ((10, 2**32 - 1), (0, 2**32 - 1), (0, 20))
+    m = O.model(thresholds=thr)
+    # outputs up to 9 tokens so that decode growth exhausts the 40-token KV (17 + 8 twice > 40)
+    combos = [(c, B, pol) for c in _tiny_cases(outs=(1, 9)) for B in (1, 3, 8)
+              for pol in (tcm.POLICY_FCFS, tcm.POLICY_TCM)]
+    tr = T.concat([T.from_requests(c) for c, _, _ in combos])
+    params = tcm.make_params(len(combos), kv_capacity=40)
+    params["chunk_budget"] = [B for _, B, _ in combos]
+    params["policy"] = [p for _, _, p in combos]
+    params["flags"] = tcm.KV_GROWTH
+    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE, thresholds=thr))
+    dev = tcm.to_device(tr, params)
+    res = tcm.alloc_results(tr.n_requests, preemption=True)
+    sim.load(dev, res)
+    sim.run()
+    out = {k: v.cpu().numpy() for k, v in res.items()}
+    npre = 0
+    for r, (c, B, pol) in enumerate(combos):
+        a, b = int(tr.offset[r]), int(tr.offset[r + 1])
+        o = O.simulate_trace_growth(tr, r, policy=int(pol), kv_capacity=40, chunk_budget=B, m=m)
+        assert o.status == 0
+        for k, v in (("admit_seq", o.admit_seq), ("first_token_us", o.first_token_us), ("done_us", o.done_us),
+                     ("preempt_count", o.preempt_count), ("preempted_us", o.preempted_us)):
+            assert out[k][a:b].tolist() == v.tolist(), (k, c, B, pol)
+        npre += o.counters["preemptions"]
+    assert npre > 0 and sim.stats()["preemptions"] == npre
+    sim.close()
