@@ -515,10 +515,12 @@ def bench_e2e(args, sw, host, dev, dist, world):
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     per_ctx = max(2, min(args.steps, 4) // 2)
     lanes = []
+    # both contexts simulate the same trace, so their per-request results are bit-identical and
+    # they share one set of pinned result buffers (host memory: 25.6 GB per rank instead of 38.7)
+    res = {"admit_seq": torch.empty(N, dtype=torch.uint32).pin_memory(),
+           "first_token_us": torch.empty(N, dtype=torch.uint64).pin_memory(),
+           "done_us": torch.empty(N, dtype=torch.uint64).pin_memory()}
     for _ in range(2):
-        res = {"admit_seq": torch.empty(N, dtype=torch.uint32).pin_memory(),
-               "first_token_us": torch.empty(N, dtype=torch.uint64).pin_memory(),
-               "done_us": torch.empty(N, dtype=torch.uint64).pin_memory()}
         st = torch.cuda.Stream(device=dev)
         sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells), st)
         lanes.append((sim, res, st))
