@@ -468,6 +468,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
       // up to kItersPerLaunch engine iterations of this replica per launch (each one the full
       // a1-a5 step); tcm_step's budget (head[1]) still bounds the total
       for (int kit = 0; kit < kItersPerLaunch; ++kit) {
+        // the replica's class pack, parameters and offset do not depend on its state: load them
+        // before the prologue so their latency overlaps the state load
+        if (wl == 0 && kit == 0) {   // stage the replica's ClassPack (144 B) in this CTA's shared memory
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(t.kpack + r);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(&sm.kp);
+            for (int q = lane; q < (int)(sizeof(ClassPack) / 4); q += 32) dst[q] = src[q];
+        }
+        const tcm_replica_params prm = t.params[r];
+        const uint64_t base = t.offset[r];
         if (wg == 0) sw_prologue<G, GR>(m, t, r, gsm, lane);
         gsync<G, CL>();
         if (gsm.mode == 0) {
@@ -476,11 +485,9 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
             break;
         }
 
-        const tcm_replica_params prm = t.params[r];
         const bool prio = prm.policy == TCM_POLICY_TCM;
         const bool edf = prm.policy == TCM_POLICY_EDF;
         const bool skip = (prm.flags & TCM_ADMIT_SKIP) != 0;
-        const uint64_t base = t.offset[r];
         // the streamed 8-byte key input: arrival (TCM aging, FCFS) or the EDF deadline x den
         const uint64_t* arr = (edf ? t.deadline : t.arrival) + base;
         const uint32_t* fp = t.footprint + base;
@@ -490,12 +497,6 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
         uint32_t* rem = remv + base;
         const uint64_t clock = gsm.st.clock;
         const bool growth = GR && (prm.flags & TCM_KV_GROWTH) != 0;
-        if (wl == 0) {   // stage the replica's ClassPack (144 B) in this CTA's shared memory
-            const uint32_t* src = reinterpret_cast<const uint32_t*>(t.kpack + r);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(&sm.kp);
-            for (int q = lane; q < (int)(sizeof(ClassPack) / 4); q += 32) dst[q] = src[q];
-            __syncwarp();
-        }
         if (wg == 0) {
             if (growth) sw_preempt(m, t, r, base, rs, rem, prio, tb, sm.kp, gsm.st, lane);
             if (lane == 0) {
