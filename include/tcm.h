@@ -75,6 +75,10 @@ enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1, TCM_POLICY_EDF = 2, TCM_POLICY_N
                                request (else TCM_E_CAPACITY).  STEPWISE only.                */
 
 enum { TCM_ENGINE_FUSED = 0, TCM_ENGINE_STEPWISE = 1 };
+/* Development knobs read from the environment at each run (not part of the contract; results are
+ * identical under every setting): TCM_SW_GROUP = 1 | 8 | cluster forces the stepwise engine's warp /
+ * CTA / 8-CTA-cluster per replica mode; TCM_FUSED_LPW = 1..32 forces the fused engine's replicas
+ * per warp. */
 /* FUSED   : one persistent thread per replica runs the whole step loop in registers;
  *           a3 is the exact 3-way merge of the class-FIFO heads (Lemma L1).
  *           Replicas must hold < 2^24 requests (calendar slot counters).

@@ -23,6 +23,7 @@
 // launch by k_fstamp from a per-replica log of (iteration, clock) events, and so are first-token
 // times: the loop itself never revisits a request once its prefill is complete.
 #include <cstdlib>
+#include <mutex>
 
 #include "tcm_internal.cuh"
 #include "tcm_k1.cuh"
@@ -803,8 +804,10 @@ void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, ui
                   cudaStream_t s) {
     // replicas per warp: the smallest power of two that keeps every replica in the resident warps
     static int cached_sms[64] = {}, cached_per_sm[64] = {};    // queried once per device
+    static std::mutex mu;                   // contexts may run concurrently from several host threads
     int dev = 0;
     cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
     if (cached_sms[dev & 63] == 0) {
         int sms = 148, per_sm = 8;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -20,6 +20,7 @@
 // Nothing here relies on Lemma L1 (class-FIFO order), so any per-request key fits this path.
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <mutex>
 
 #include "tcm_k1.cuh"
 #include "tcm_stepwise.cuh"
@@ -1116,8 +1117,10 @@ struct DevFacts {
 
 DevFacts dev_facts() {
     static DevFacts cache[64];
+    static std::mutex mu;                   // contexts may step concurrently from several host threads
     int dev = 0;
     cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
     DevFacts& f = cache[dev & 63];
     if (f.sms == 0) {
         int sms = 148;
