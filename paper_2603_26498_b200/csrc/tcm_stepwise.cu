@@ -730,12 +730,14 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 const uint64_t a4[4] = {v0.x, v0.y, v1.x, v1.y};
                 const uint32_t s4 = rst[slot * 32 + lane];
                 const int e0 = (int)(g0 + 4 * lane);
+                bool take_chunk = true;
                 if (lean) {
                     // fast rejection: arrivals after every class's limit, and no partial to record
                     // (arrivals are sorted, so a lane's first element is its smallest)
                     const bool maybe = (first_pass && (s4 & 0x08080808u) != 0) || (int64_t)a4[0] <= amx;
-                    if (!__any_sync(0xFFFFFFFFu, maybe)) continue;
+                    take_chunk = __any_sync(0xFFFFFFFFu, maybe);
                 }
+                if (take_chunk) {
                 uint32_t qbits = 0;                       // bit j: element j goes to the refine queue
                 bool any_direct = false;
 #pragma unroll
@@ -769,12 +771,14 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                     }
                 }
                 if (!prio && __any_sync(0xFFFFFFFFu, any_direct)) {
-#pragma unroll
+                    // not unrolled: one inlined copy of take() instead of four (instruction cache)
+#pragma unroll 1
                     for (int j = 0; j < 4; ++j) {
                         const int e = e0 + j;
                         const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
                         const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
-                        const uint64_t key = edf ? ~a4[j] : 0;
+                        const uint64_t aj = j == 0 ? a4[0] : (j == 1 ? a4[1] : (j == 2 ? a4[2] : a4[3]));
+                        const uint64_t key = edf ? ~aj : 0;
                         take(key, (uint32_t)e, valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
                                                   before(key, (uint32_t)e, kk, ki));
                     }
@@ -801,17 +805,22 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                     }
                     qn += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
                     __syncwarp();
-                    while (qn >= 32) {                       // the queue is a ring: no shifting
-                        refine(32);
-                        qh += 32;
-                        qh -= qh >= kQ ? kQ : 0;
-                        qn -= 32;
-                        __syncwarp();
-                    }
+                }
+                }   // take_chunk
+                // refine full batches; after the last chunk also the remainder.  One call site of
+                // refine (and take) keeps the kernel small for the instruction cache.  The queue is
+                // a ring: no shifting.
+                const bool last = g0 + stride >= (int64_t)hi;
+                while (qn >= 32 || (last && qn > 0)) {
+                    const int cnt = qn < 32 ? qn : 32;
+                    refine(cnt);
+                    qh += cnt;
+                    qh -= qh >= kQ ? kQ : 0;
+                    qn -= cnt;
+                    __syncwarp();
                 }
             }
             cp_async_wait<0>();
-            if (qn > 0) refine(qn);
             if (G > 1) {
                 sm.wkey[wl][lane] = lk;
                 sm.wid[wl][lane] = li;
