@@ -678,7 +678,8 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 if (!__any_sync(0xFFFFFFFFu, live)) return;
                 if (live) {
                     const int c = cc & RS_CLS;
-                    key = prio ? k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qwl, tb) : 0;
+                    key = prio ? k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qwl, tb)
+                               : (edf ? ~(clock - qwl) : 0);     // EDF: ~(deadline x den); FCFS / aging: 0
                     if (first_pass && (cc & RS_RES)) {                 // partial: remember its key
                         const int slot = atomicAdd(&gsm.npart, 1);
                         if (slot < kMaxPart) {
@@ -739,7 +740,6 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 }
                 if (take_chunk) {
                 uint32_t qbits = 0;                       // bit j: element j goes to the refine queue
-                bool any_direct = false;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int e = e0 + j;
@@ -756,31 +756,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                     } else if (!prio) {
                         // exact keys without K1: FCFS / naive aging (key 0, id order, R4) or EDF
                         // (static key ~(deadline x den): earliest deadline first)
+                        // queued like TCM candidates (refine recomputes the key from the queued
+                        // value and registers partials); partials always, on the first pass
                         const uint64_t key = edf ? ~a4[j] : 0;
-                        any_direct |= valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
-                                      before(key, (uint32_t)e, kk, ki);
-                        if (valid && first_pass && (sb & RS_RES)) {
-                            const int slot = atomicAdd(&gsm.npart, 1);
-                            if (slot < kMaxPart) {
-                                gsm.part[slot] = (uint32_t)e;
-                                gsm.partkey[slot] = key;
-                            }
-                        }
+                        const bool need = valid && ((first_pass && (sb & RS_RES)) ||
+                                                    (!(has_th && !before(thk, thi, key, (uint32_t)e)) &&
+                                                     before(key, (uint32_t)e, kk, ki)));
+                        qbits |= need ? (1u << j) : 0u;
                     } else {
                         qbits |= valid ? (1u << j) : 0u;     // exact key for every pending request
-                    }
-                }
-                if (!prio && __any_sync(0xFFFFFFFFu, any_direct)) {
-                    // not unrolled: one inlined copy of take() instead of four (instruction cache)
-#pragma unroll 1
-                    for (int j = 0; j < 4; ++j) {
-                        const int e = e0 + j;
-                        const uint32_t sb = (s4 >> (8 * j)) & 0xFF;
-                        const bool valid = (sb & RS_PEND) && e >= (int)lo && e < (int)hi;
-                        const uint64_t aj = j == 0 ? a4[0] : (j == 1 ? a4[1] : (j == 2 ? a4[2] : a4[3]));
-                        const uint64_t key = edf ? ~aj : 0;
-                        take(key, (uint32_t)e, valid && !(has_th && !before(thk, thi, key, (uint32_t)e)) &&
-                                                  before(key, (uint32_t)e, kk, ki));
                     }
                 }
                 if (__any_sync(0xFFFFFFFFu, qbits != 0)) {
