@@ -166,7 +166,7 @@ typedef struct tcm_stats_host {
     double reset_ms;           /* the reset: memsets, state init, engine prologue (FUSED: the
                                   class-segment build, row a1)                            */
     double engine_ms;          /* the step kernels (FUSED: k_fused; STEPWISE: the k_step
-                                  launches, one per engine iteration)                      */
+                                  launches, each up to 16 engine iterations per replica)    */
     double stamp_ms;           /* FUSED: k_fstamp (first-token / finish times from the log) */
     uint64_t preemptions;      /* TCM_KV_GROWTH: preemptions (R29)                     */
     uint64_t forced_preemptions; /* TCM: motorcycle victims (only when nothing else ran)  */

@@ -1,23 +1,28 @@
 // tcm_stepwise.cu -- TCM_ENGINE_STEPWISE: the paper-literal per-iteration scheduling step.
 //
-// Every engine iteration, for every active replica, one GROUP of G warps (G = 1: a warp per
-// replica, for sweeps of many replicas; G = 8: a CTA per replica, for a few huge queues):
+// Every engine iteration, for every active replica, one GROUP of warps (a warp per replica for
+// sweeps; a CTA for fewer, huge queues; a thread-block cluster of 8 CTAs for a handful of huge
+// queues, its group state in rank 0's shared memory through DSMEM):
 //   a1  ingests arrivals <= clock (ballots over 128 sorted arrivals per round) and classifies
 //       them (R13) into the per-request state byte;
-//   a2  re-keys EVERY pending request of the replica's window [lo, nxt) with K1
-//       ("At each scheduling iteration ... evaluates the state of all queues and dynamically
-//       adjusts priorities"): a coalesced, vectorised, software-pipelined
-//       SoA stream of arrival (8 B) + state (1 B) per request; the key is never stored;
-//   a3  selects the top-32 candidates by (key desc, id asc): per-warp register lists updated
-//       by warp-shuffle bitonic networks (a ballot skips batches that cannot enter), merged
-//       across the group's warps through shared memory;
-//   a4  admits by warp-shuffle prefix scans of footprints against free KV and of chunk tokens
+//   a2  streams EVERY pending request of the replica's window [lo, nxt) ("At each scheduling
+//       iteration ... evaluates the state of all queues and dynamically adjusts priorities",
+//       PAPER.md:315, 323): arrival (8 B) + state (1 B) per request through a per-warp cp.async
+//       ring; a request is rejected by a per-class arrival limit derived from one FP32 bound of
+//       K1 (monotone in the waiting time), else queued, in id order, for its exact K1 key;
+//       the key is never stored;
+//   a3  selects the top-32 candidates by (key desc, id asc): per-warp register lists updated by
+//       ballot-rank insertion or warp-shuffle bitonic networks (compound 64-bit keys for TCM),
+//       merged across the group's warps through shared memory;
+//   a4  admits by warp-shuffle prefix scans of KV needs against free KV and of chunk tokens
 //       against the budget (R5-R8); if the scan has not terminated after 32 candidates it
 //       re-streams for the next 32 (threshold = last selected); partials ranked below a KV
 //       block keep their chunks (R6);
 //   a5  advances the clock, stamps first tokens and runs the decode calendar (same integer
 //       arithmetic as the fused engine), with the decode-only fast-forward (Lemma L3).
-// Nothing here relies on Lemma L1 (class-FIFO order), so any per-request key fits this path.
+// NEXT-1 (TCM_KV_GROWTH, R28-R32): sw_preempt before a4, re-admissions in a4, token accounting
+// in a5.  The order never relies on Lemma L1 (class-FIFO order), so any per-request key fits
+// this path; the FP32 filter uses only K1's monotonicity.
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <mutex>
