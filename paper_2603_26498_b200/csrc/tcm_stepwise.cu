@@ -74,7 +74,7 @@ __device__ __forceinline__ bool before(uint64_t ka, uint32_t ia, uint64_t kb, ui
 }
 
 // Bitonic sort of one (key, id) per lane, descending across lanes 0..31.
-__device__ __forceinline__ void warp_sort_desc(uint64_t& k, uint32_t& i, int lane) {
+__device__ __forceinline__ void warp_sort_desc_il(uint64_t& k, uint32_t& i, int lane) {
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
@@ -95,7 +95,7 @@ __device__ __forceinline__ void warp_sort_desc(uint64_t& k, uint32_t& i, int lan
 
 // Merge a descending batch into a descending list, keeping the top 32: element-wise max with
 // the reversed batch gives a bitonic sequence holding the top 32; clean it.
-__device__ __forceinline__ void warp_merge(uint64_t& lk, uint32_t& li, uint64_t bk, uint32_t bi, int lane) {
+__device__ __forceinline__ void warp_merge_il(uint64_t& lk, uint32_t& li, uint64_t bk, uint32_t bi, int lane) {
     const uint64_t rk = __shfl_sync(0xFFFFFFFFu, bk, 31 - lane);
     const uint32_t ri = __shfl_sync(0xFFFFFFFFu, bi, 31 - lane);
     if (before(rk, ri, lk, li)) {
@@ -112,6 +112,31 @@ __device__ __forceinline__ void warp_merge(uint64_t& lk, uint32_t& li, uint64_t 
             li = pi;
         }
     }
+}
+
+// Out-of-line copies of the generic (key, id) networks: they sit off the TCM hot path (compound
+// keys), so one copy each keeps k_step small for the instruction cache.  Values in and out.
+struct KeyId {
+    uint64_t k;
+    uint32_t i;
+};
+__device__ __noinline__ KeyId warp_sort_desc_ool(uint64_t k, uint32_t i, int lane) {
+    warp_sort_desc_il(k, i, lane);
+    return KeyId{k, i};
+}
+__device__ __noinline__ KeyId warp_merge_ool(uint64_t lk, uint32_t li, uint64_t bk, uint32_t bi, int lane) {
+    warp_merge_il(lk, li, bk, bi, lane);
+    return KeyId{lk, li};
+}
+__device__ __forceinline__ void warp_sort_desc(uint64_t& k, uint32_t& i, int lane) {
+    const KeyId r = warp_sort_desc_ool(k, i, lane);
+    k = r.k;
+    i = r.i;
+}
+__device__ __forceinline__ void warp_merge(uint64_t& lk, uint32_t& li, uint64_t bk, uint32_t bi, int lane) {
+    const KeyId r = warp_merge_ool(lk, li, bk, bi, lane);
+    lk = r.k;
+    li = r.i;
 }
 
 // Compound-key variants for TCM keys (bit patterns of P in [1e-12, 2^17), so key - kKeyBase < 2^58):
