@@ -193,8 +193,9 @@ __global__ void __launch_bounds__(256) k_aggregate(ModelConst m, TraceDev t, uns
             const uint64_t arr = t.arrival[i];
             const uint64_t ttft = t.first_token[i] - arr;
             const uint64_t e2e = t.done[i] - arr;
-            const uint64_t iso = (uint64_t)t.inl[i] + ((uint64_t)f + B - 1) / B * m.c0 + m.cp * f +
-                                 (uint64_t)(o - 1) * (m.c0 + m.cd);
+            const uint32_t B32 = (uint32_t)B;              // ceil(f / B) in 32-bit integer division
+            const uint64_t nch = f / B32 + (f % B32 != 0);
+            const uint64_t iso = (uint64_t)t.inl[i] + nch * m.c0 + m.cp * f + (uint64_t)(o - 1) * (m.c0 + m.cd);
             const uint64_t lhs = e2e * m.slo_den, rhs = iso * m.slo_num;
             const bool viol = lhs > rhs;
             const uint32_t bk = ttft_bucket(ttft);
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(256) k_aggregate(ModelConst m, TraceDev t, uns
                     c[q][2] += e2e;
                     c[q][3] += viol ? 1 : 0;
                     c[q][4] += viol ? lhs - rhs : 0;
-                    c[q][5] += e2e / o;
+                    c[q][5] += e2e < (1ull << 32) ? (uint64_t)((uint32_t)e2e / o) : e2e / o;   // 32-bit when it fits
                 }
             }
         }
