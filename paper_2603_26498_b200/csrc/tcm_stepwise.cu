@@ -467,7 +467,8 @@ __device__ __noinline__ void sw_preempt(const ModelConst& m, const TraceDev& t, 
 // the growth code out of the hot path.
 template <int G, bool GR, int CL>
 __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
-                                                      int count_active) {
+                                                      int count_active, unsigned long long* ctr,
+                                                      unsigned long long ctr_base) {
     constexpr int kGroups = kWarpsPerBlock / G;
     constexpr int kMaxDone = GroupSmem<G>::kMaxDone;
     __shared__ double s_lnR[16], s_lnT[16], s_expT[16];
@@ -495,7 +496,17 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
 
     const uint32_t r0 = CL > 1 ? blockIdx.x / CL : blockIdx.x * kGroups + group;
     const uint32_t rstep = CL > 1 ? gridDim.x / CL : gridDim.x * kGroups;
-    for (uint32_t r = r0; r < t.R; r += rstep) {
+    // A warp per replica takes replicas from a global counter (dynamic balance; every warp of the
+    // launch ends with exactly one failing grab, so a launch advances the counter by R + warps and
+    // the host passes each launch its base); CTA and cluster groups use a static stride.
+    const bool kDyn = G == 1 && CL == 1 && ctr != nullptr;   // host passes nullptr when R <= warps
+    auto grab = [&]() -> uint32_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(ctr, 1ull) - ctr_base;
+        v = __shfl_sync(0xFFFFFFFFu, v, 0);
+        return v < t.R ? (uint32_t)v : t.R;
+    };
+    for (uint32_t r = kDyn ? grab() : r0; r < t.R; r = kDyn ? grab() : r + rstep) {
       // up to kItersPerLaunch engine iterations of this replica per launch (each one the full
       // a1-a5 step); tcm_step's budget (head[1]) still bounds the total
       for (int kit = 0; kit < kItersPerLaunch; ++kit) {
@@ -1206,7 +1217,14 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
                         uint32_t* d_active, cudaStream_t s, uint64_t* launches, cudaEvent_t ev_begin,
                         cudaEvent_t ev_end, double* kernel_ms) {
     uint32_t* remv = reinterpret_cast<uint32_t*>(w.base);
+    // replica counter for the warp-per-replica mode: in the workspace's 16 spare bytes after rem
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(w.base) + ((4 * t.N + 7) & ~7ull));
     const Launch L = stepwise_config(t.R, t.N);
+    const unsigned long long per_launch = (unsigned long long)t.R + (unsigned long long)L.grid * kWarpsPerBlock;
+    if (L.group != 1 || L.cluster != 1 || t.R <= (uint64_t)L.grid * kWarpsPerBlock) ctr = nullptr;   // static is ideal
+    unsigned long long ctr_base = 0;
+    if (ctr && cudaMemsetAsync(ctr, 0, 8, s) != cudaSuccess) return TCM_E_CUDA;
     k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, max_iters);
     (*launches)++;
     // Each k_step launch advances every active replica by one iteration (or one fast-forward);
@@ -1235,17 +1253,18 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
                 cudaError_t e = t.any_growth
-                    ? cudaLaunchKernelEx(&cfg, k_step<8, true, kCluster>, m, t, remv, d_active, last)
-                    : cudaLaunchKernelEx(&cfg, k_step<8, false, kCluster>, m, t, remv, d_active, last);
+                    ? cudaLaunchKernelEx(&cfg, k_step<8, true, kCluster>, m, t, remv, d_active, last, ctr, ctr_base)
+                    : cudaLaunchKernelEx(&cfg, k_step<8, false, kCluster>, m, t, remv, d_active, last, ctr, ctr_base);
                 if (e != cudaSuccess) return TCM_E_CUDA;
             } else if (t.any_growth) {
-                if (L.group == 1) k_step<1, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
-                else k_step<8, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+                if (L.group == 1) k_step<1, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
+                else k_step<8, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
             } else {
-                if (L.group == 1) k_step<1, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
-                else k_step<8, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last);
+                if (L.group == 1) k_step<1, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
+                else k_step<8, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
             }
             (*launches)++;
+            ctr_base += per_launch;
         }
         done_launches += this_chunk;
         if (cudaEventRecord(ev_end, s) != cudaSuccess) return TCM_E_CUDA;
