@@ -49,7 +49,7 @@ constexpr uint8_t RS_DEC = 32, RS_PREV = 64, RS_GEN = 128;
 
 // stream staging: per warp, kStages chunks of 128 requests (1 KB arrivals + 128 B states)
 #ifndef TCM_SW_STAGES
-#define TCM_SW_STAGES 3
+#define TCM_SW_STAGES 4
 #endif
 #ifndef TCM_SW_MINB
 #define TCM_SW_MINB 3
