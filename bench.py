@@ -31,13 +31,21 @@ sys.path.insert(0, ROOT)
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0           # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
 
-# algorithmic bytes of k_fused per simulated request: class record read (32), arrival
-# stream (8), admit_seq (4), first-token iteration (8), finish iteration (8), calendar slot
-# reduction (8), event-log entry (16); per replica: state r+w, class constants, params, occupancy
-FUSED_BYTES_PER_REQ = 32 + 8 + 4 + 8 + 8 + 8 + 16
-FUSED_BYTES_PER_REPLICA = 256 + 144 + 32 + 256
+# Algorithmic bytes of the path per simulated request: the trace SoA read once
+# (arrival 8 + footprint 4 + inline 4 + out 2 + modality 1 = 19 B), the results written once
+# (admit_seq 4 + first_token 8 + done 8 = 20 B) and the decode-calendar update (~16 B); per replica
+# the 128 B state read + written.  k_fused's own workspace traffic (class records, event log, finish
+# iterations: DESIGN.md 7) is implementation overhead and is reported apart, not counted.
+ALG_BYTES_PER_REQ = 19 + 20 + 16
+ALG_BYTES_PER_REPLICA = 256
+FUSED_WS_BYTES_PER_REQ = 32 + 16 + 8 + 8     # record read + event log + finish iteration + record write
 STEP_BYTES_PER_PENDING = 9                 # stepwise: arrival (8) + state byte (1) per pending key
 STEP_BYTES_PER_DECISION = 256              # replica state r+w
+
+# One metric string per workload, identical on both arms (the driver divides the two lines).
+METRIC = {w: f"simulated requests/sec ({w.upper()} sweep)" for w in ("c3", "c4", "c5")}
+METRIC["c4"] = "simulated requests/sec (C4 memory-pressure sweep)"
+METRIC["c1"] = "simulated requests/sec (C1 single trace)"
 
 
 def peak_hbm():
@@ -93,15 +101,65 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """`bench.py --gpus N` (N > 1) run without a launcher re-executes itself under torchrun with N
+    ranks (one process per GPU, rendezvous on 127.0.0.1).  Returns the exit code, or None when this
+    process is already a rank (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")              # communicator-init lines (rank count, transport)
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/tmp/tcm_bench_nccl.%h.%p.log")   # keep stdout to the JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    log("spawning:", " ".join(cmd))
+    return subprocess.call(cmd, env=env)
+
+
 def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "tcm" else "gloo"
-        dist.init_process_group(backend=backend)
+        if args.impl == "tcm":
+            import torch
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend="gloo")
+        assert dist.get_world_size() == args.gpus
     return rank, world, local
+
+
+def nccl_evidence():
+    """NCCL version and the communicator-init lines NCCL_DEBUG=INFO wrote (rank 0's view)."""
+    import glob
+    out = {}
+    try:
+        import torch
+        out["version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+    except Exception:
+        pass
+    lines = []
+    for f in sorted(glob.glob("/tmp/tcm_bench_nccl.*.log")):
+        try:
+            lines += [ln.strip() for ln in open(f) if "Init COMPLETE" in ln or "nranks" in ln][:4]
+        except OSError:
+            pass
+    if lines:
+        out["init_lines"] = lines[:16]
+    return out
 
 
 # ----------------------------------------------------------------------------------- oracle
@@ -119,61 +177,121 @@ def _oracle_job(job):
     return dt, n, r.counters["decisions"]
 
 
-def oracle_sample(sweep, n_trunc=1000, per_cell=1, cells_sel=None):
-    """Time the oracle (as it stands) on a bounded sample of the sweep: `per_cell` replicas of
-    every cell, truncated to their first n_trunc requests, one replica per process on the host
-    cores."""
-    import multiprocessing as mp
+def cpu_model():
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def sample_ids(sweep, n_sample):
+    """A deterministic sample spread over the sweep: every (R / n_sample)-th replica (replicas are
+    ordered cell-major, so the sample covers every cell in equal measure)."""
     R = sweep.n_replicas
-    cells = sweep.params["cell_id"]
-    idx = []
-    for c in (range(sweep.n_cells) if cells_sel is None else cells_sel):
-        idx.extend(np.nonzero(cells == c)[0][:per_cell].tolist())
+    step = max(1, R // n_sample)
+    return list(range(step // 2, R, step))[:n_sample]
+
+
+def oracle_sample(sweep, n_trunc=0, n_sample=64, cores=None):
+    """Time the oracle (as it stands) on a bounded sample of the sweep: n_sample replicas spread
+    over every cell (sample_ids), each truncated to its first n_trunc requests (0 = full length),
+    one single-threaded oracle process per replica on `cores` host cores (all by default).
+    Returns the all-core wall time and the sum of the per-replica (1-core) times."""
+    import multiprocessing as mp
+    idx = sample_ids(sweep, n_sample)
     jobs = [(sweep.gen[i], int(sweep.params[i]["policy"]), int(sweep.params[i]["kv_capacity"]),
-             float(sweep.params[i]["aging_alpha"]), int(sweep.params[i]["chunk_budget"]), n_trunc) for i in idx]
-    cores = min(len(jobs), os.cpu_count() or 1)
+             float(sweep.params[i]["aging_alpha"]), int(sweep.params[i]["chunk_budget"]),
+             n_trunc or int(sweep.gen[i]["n_requests"])) for i in idx]
+    cores = min(len(jobs), cores or os.cpu_count() or 1)
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(cores) as pool:     # never fork a CUDA process
         res = pool.map(_oracle_job, jobs, chunksize=1)
     wall = time.perf_counter() - t0
     nreq = sum(r[1] for r in res)
     ndec = sum(r[2] for r in res)
+    cpu_s = sum(r[0] for r in res)
     return {"wall_s": wall, "requests": nreq, "decisions": ndec, "cores": cores, "replicas": len(jobs),
-            "n_trunc": n_trunc}
+            "n_trunc": n_trunc, "one_core_s": cpu_s, "max_replica_s": max(r[0] for r in res)}
+
+
+def cpu_baseline_line(s, workload):
+    length = f"first {s['n_trunc']} requests each" if s["n_trunc"] else "full length"
+    return {"value": s["requests"] / s["wall_s"], "unit": "requests/s", "cores": s["cores"], "kind": "oracle",
+            "decisions_per_s": s["decisions"] / s["wall_s"],
+            "one_core_value": s["requests"] / s["one_core_s"],
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "sample": f"{s['replicas']} {workload.upper()} replicas spread over every cell (every "
+                      f"R/{s['replicas']}-th replica), {length}, one single-threaded oracle process per replica on "
+                      f"{s['cores']} host cores: {s['wall_s']:.1f} s wall (all-core value), "
+                      f"{s['one_core_s']:.1f} s summed per-replica time (one_core_value)"}
 
 
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle on the box's host cores (rank 0 only)."""
     if rank != 0:
         return
-    from paper_2603_26498_b200 import workloads as W
-    sw = W.c4(0, 1, replicas_per_gpu=args.replicas, n_requests=args.requests)
+    sw = make_sweep(args, 0, 1)
+    n_sample = min(32, sw.n_replicas)
     for _ in range(args.warmup):
-        oracle_sample(sw, n_trunc=args.ref_requests)
+        oracle_sample(sw, n_trunc=args.ref_requests, n_sample=n_sample)
     tot_req = tot_dec = 0
-    tot_wall = 0.0
-    cores = 0
+    tot_wall = tot_one = 0.0
+    s = None
     for _ in range(args.steps):
-        s = oracle_sample(sw, n_trunc=args.ref_requests)
+        s = oracle_sample(sw, n_trunc=args.ref_requests, n_sample=n_sample)
         tot_req += s["requests"]
         tot_dec += s["decisions"]
         tot_wall += s["wall_s"]
-        cores = s["cores"]
+        tot_one += s["one_core_s"]
     v = tot_req / tot_wall
-    sample = (f"one replica of each of the 32 C4 cells, first {args.ref_requests} requests each, "
-              f"one oracle process per replica on {cores} host cores")
+    cb = cpu_baseline_line(dict(s, requests=tot_req, decisions=tot_dec, wall_s=tot_wall, one_core_s=tot_one),
+                           args.workload)
     line = {
-        "impl": "reference", "metric": "simulated requests/sec (C4 memory-pressure sweep)", "value": v,
+        "impl": "reference", "metric": METRIC[args.workload], "value": v,
         "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
         "decisions_per_s": tot_dec / tot_wall,
-        "config": {"workload": "C4 memory-pressure sweep (bounded oracle sample)", "replicas": 32,
-                   "requests_per_replica": args.ref_requests},
-        "cpu_baseline": {"value": v, "unit": "requests/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "config": {"workload": f"{workload_name(args, sw)} (bounded oracle sample: {n_sample} replicas, first "
+                               f"{args.ref_requests} requests each)",
+                   "replicas": n_sample, "requests_per_replica": args.ref_requests},
+        "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def make_sweep(args, rank, world):
+    from paper_2603_26498_b200 import workloads as W
+    if args.workload == "c5":
+        # C5 (BASELINE.json configs[4]): 1M replicas on 8 GPUs = 131,072 per GPU (weak scaling)
+        return W.c5(rank, world, replicas=args.replicas * world, n_requests=args.requests)
+    if args.workload == "c3":
+        # C3 (configs[2]): 4,096 replicas x 10k, lambda x alpha sweep, per GPU
+        return W.c3(rank, world, replicas=args.replicas * world, n_requests=args.requests)
+    if args.workload == "c1":
+        # C1 (configs[0]): one replica x 1,000 requests (TCM), a single serial engine per GPU; rank k
+        # simulates seed 1 + k so that ranks never count the same replica twice
+        return W.c1(seed=1 + rank)
+    return W.c4(rank, world, replicas_per_gpu=args.replicas, n_requests=args.requests)
+
+
+def workload_name(args, sw):
+    R = sw.n_replicas
+    if args.workload == "c3":
+        return (f"C3 sweep: {R} replicas x {args.requests} requests per GPU (16 lambda x 16 alpha x seeds, 70/25/5, "
+                "TCM), fused engine")
+    if args.workload == "c1":
+        return "C1: 1 replica x 1,000 requests per GPU (70/25/5, 2 req/s, TCM), fused engine: one serial engine"
+    if args.workload == "c5":
+        return (f"C5 full policy sweep: {R} replicas x {args.requests} requests per GPU (16 lambda x 8 mixes x 16 "
+                f"alpha x 8 chunk budgets = {sw.n_cells} cells x seeds; 1M replicas at 8 GPUs), fused engine, "
+                "per-request results kept in the library workspace")
+    return (f"C4 memory-pressure sweep: {args.replicas} replicas x {args.requests} requests per GPU "
+            "(50/20/30 mix, KV 128k..16k x lambda 0.5..4 x FCFS/TCM), fused engine")
 
 
 # ------------------------------------------------------------------------------------ GPU
@@ -190,17 +308,7 @@ def run_tcm(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
 
-    if args.workload == "c5":
-        # C5 (BASELINE.json configs[4]): 1M replicas on 8 GPUs = 131,072 per GPU (weak scaling)
-        sw = W.c5(rank, world, replicas=args.replicas * world, n_requests=args.requests)
-    elif args.workload == "c3":
-        # C3 (configs[2]): 4,096 replicas x 10k, lambda x alpha sweep, per GPU
-        sw = W.c3(rank, world, replicas=args.replicas * world, n_requests=args.requests)
-    elif args.workload == "c1":
-        # C1 (configs[0]): one replica x 1,000 requests (TCM), a single serial engine per GPU
-        sw = W.c1()
-    else:
-        sw = W.c4(rank, world, replicas_per_gpu=args.replicas, n_requests=args.requests)
+    sw = make_sweep(args, rank, world)
     R, N = sw.n_replicas, sw.n_requests
     log(f"rank {rank}: {args.workload.upper()} shard {R} replicas, {N} requests; generating on device")
     with torch.cuda.stream(stream):
@@ -211,8 +319,9 @@ def run_tcm(args, rank, world, local):
     cfg = tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells)
     sim = tcm.Simulation(cfg, stream)
     sim.load(trace, results)
-    hist = torch.zeros((sw.n_cells, tcm.GROUPS, tcm.HIST_BINS), dtype=torch.int64, device=dev)
-    cnt = torch.zeros((sw.n_cells, tcm.GROUPS, tcm.NCNT), dtype=torch.int64, device=dev)
+    with torch.cuda.stream(stream):        # tcm_stats overwrites them on the library's stream
+        hist = torch.empty((sw.n_cells, tcm.GROUPS, tcm.HIST_BINS), dtype=torch.int64, device=dev)
+        cnt = torch.empty((sw.n_cells, tcm.GROUPS, tcm.NCNT), dtype=torch.int64, device=dev)
 
     def one_step():
         sim.reset()
@@ -261,7 +370,8 @@ def run_tcm(args, rank, world, local):
 
     # max over ranks of the device time; totals over ranks
     tot = torch.tensor([float(N * args.steps), float(st1["decisions"] * args.steps),
-                        float(st1["iterations"] * args.steps)], dtype=torch.float64, device=dev)
+                        float(st1["iterations"] * args.steps), float(st1["scanned_decisions"] * args.steps)],
+                       dtype=torch.float64, device=dev)
     mx = torch.tensor([ms, max(run_ms)], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(tot)
@@ -270,39 +380,42 @@ def run_tcm(args, rank, world, local):
     req_s = float(tot[0]) / (ms_max / 1e3)
     dec_s = float(tot[1]) / (ms_max / 1e3)
 
-    # roofline of the dominant kernel (k_fused): algorithmic bytes per launch / its launch time,
-    # from CUDA events the library records around the launch on this stream
+    scan_s = float(tot[3]) / (ms_max / 1e3)
+    # roofline of the dominant kernel (k_fused): SURVEY.md 8(d)'s algorithmic bytes per launch / its
+    # launch time, from CUDA events the library records around the launch on this stream
     peak, peak_kind = peak_hbm()
     fused_ms = float(np.mean([k[1] for k in kms]))
-    alg_bytes = N * FUSED_BYTES_PER_REQ + R * FUSED_BYTES_PER_REPLICA
+    alg_bytes = N * ALG_BYTES_PER_REQ + R * ALG_BYTES_PER_REPLICA
     achieved = alg_bytes / (fused_ms / 1e3) / 1e9
-    traffic = None
+    traffic = issue = None
     prof = os.path.join(ROOT, "profiles", "fused_dram_bytes.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.workload == "c4":
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_request")
             traffic = traffic * N if traffic else None
         except Exception:
             traffic = None
+    # issue-rate roof of the same kernel (it is latency/divergence-bound, not HBM-bound): executed
+    # warp instructions of one launch (ncu, committed profile) / (148 SMs x 4 schedulers x SM clock)
+    prof = os.path.join(ROOT, "profiles", "fused_issue.json")
+    if os.path.exists(prof) and args.workload == "c4":
+        try:
+            pi = json.load(open(prof))
+            slots = 148 * 4 * pi["sm_clock_hz"] * (fused_ms / 1e3)
+            issue = {"inst_executed_per_launch": pi["inst_executed"], "issue_slots_per_launch": slots,
+                     "frac": pi["inst_executed"] / slots,
+                     "thread_inst_per_inst": pi.get("thread_inst_per_inst"), "source": pi.get("source")}
+        except Exception:
+            issue = None
 
-    if args.workload == "c3":
-        wl = (f"C3 sweep: {R} replicas x {args.requests} requests per GPU (16 lambda x 16 alpha x seeds, 70/25/5, "
-              "TCM), fused engine")
-    elif args.workload == "c1":
-        wl = "C1: 1 replica x 1,000 requests (70/25/5, 2 req/s, TCM), fused engine: one serial engine, latency-bound"
-    elif args.workload == "c5":
-        wl = (f"C5 full policy sweep: {R} replicas x {args.requests} requests per GPU (16 lambda x 8 mixes x 16 alpha x "
-              f"8 chunk budgets = {sw.n_cells} cells x seeds; 1M replicas at 8 GPUs), fused engine, per-request results "
-              "kept in the library workspace")
-    else:
-        wl = (f"C4 memory-pressure sweep: {args.replicas} replicas x {args.requests} requests per GPU "
-              "(50/20/30 mix, KV 128k..16k x lambda 0.5..4 x FCFS/TCM), fused engine")
+    wl = workload_name(args, sw)
     out = {
-        "metric": f"simulated requests/sec ({args.workload.upper()} sweep); decisions/sec alongside",
+        "metric": METRIC[args.workload],
         "value": req_s, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
         "decisions_per_s": dec_s,
+        "scanned_decisions_per_s": scan_s,
         "config": {"workload": wl, "n_cells": sw.n_cells,
                    "replicas_per_gpu": args.replicas, "requests_per_replica": args.requests,
                    "requests_per_step": int(tot[0] / args.steps), "parallelism": f"replicas sharded x{world}",
@@ -310,7 +423,12 @@ def run_tcm(args, rank, world, local):
         "roofline": {"kernel": "k_fused", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "launch_ms": fused_ms, "alg_bytes_per_launch": alg_bytes,
-                     "note": "latency-bound per-replica chains; HBM is not the binding roof (DESIGN.md 7)"},
+                     "alg_bytes_per_request": ALG_BYTES_PER_REQ,
+                     "workspace_bytes_per_launch": N * FUSED_WS_BYTES_PER_REQ,
+                     "issue": issue,
+                     "note": "SURVEY.md 8(d) algorithmic bytes (trace 19 + results 20 + calendar 16 B per request); "
+                             "the kernel is bound by per-replica dependent chains and SIMT divergence, so the issue "
+                             "roof is reported alongside (DESIGN.md 7)"},
         "kernel_ms_per_step": {"reset_and_prologue": float(np.mean([k[0] for k in kms])), "k_fused": fused_ms,
                                "k_fstamp": float(np.mean([k[2] for k in kms]))},
         "gpu_launches": int(launches_per_step * args.steps),
@@ -336,22 +454,28 @@ def run_tcm(args, rank, world, local):
     if not args.skip_e2e:
         # free the device-resident run first: the two e2e contexts need ~74 GB each
         host = host_copy(trace)
+        # a sample of the device-resident run's results: the e2e leg's outputs are checked against it
+        pick = torch.arange(0, N, 997, device=dev)
+        ref = {k: results[k][pick].cpu().numpy() for k in ("admit_seq", "first_token_us", "done_us")}
         sim.close()
         del trace, results
         torch.cuda.empty_cache()
-        out["e2e"] = bench_e2e(args, sw, host, dev, dist, world)
+        out["e2e"] = bench_e2e(args, sw, host, dev, dist, world, (pick.cpu().numpy(), ref))
         del host
     log("e2e done")
 
     if rank == 0 and world == 1 and not args.skip_cpu:      # the oracle baseline: rank 0 at N=1 only
-        sel = None if sw.n_cells <= 64 else list(range(0, sw.n_cells, sw.n_cells // 32))   # C5: 32 spread cells
-        s = oracle_sample(sw, n_trunc=args.ref_requests, cells_sel=sel)
-        out["cpu_baseline"] = {"value": s["requests"] / s["wall_s"], "unit": "requests/s", "cores": s["cores"],
-                               "kind": "oracle",
-                               "decisions_per_s": s["decisions"] / s["wall_s"],
-                               "sample": f"{s['replicas']} {args.workload.upper()} replicas (one per sampled cell), first "
-                                         f"{s['n_trunc']} requests each, one oracle process per replica, "
-                                         f"{s['wall_s']:.1f} s wall"}
+        s = oracle_sample(sw, n_trunc=0 if args.cpu_full else args.ref_requests,
+                          n_sample=min(64, sw.n_replicas))
+        out["cpu_baseline"] = cpu_baseline_line(s, args.workload)
+        prof = os.path.join(ROOT, "profiles", f"cpu_baseline_full_{args.workload}.json")
+        if not args.cpu_full and os.path.exists(prof):
+            try:     # the full-length sample, measured once on this box type (bench.py --cpu-full)
+                out["cpu_baseline_full_length"] = json.load(open(prof))
+            except Exception:
+                pass
+    if world > 1 and rank == 0:
+        out["nccl"] = nccl_evidence()
     sim.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -401,7 +525,7 @@ def time_steps(sim, stream, iters, reps):
                 calls.append(e0.elapsed_time(e1))
                 times.append(s1["engine_ms"] - s0["engine_ms"])
                 pend.append(s1["sum_pending"] - s0["sum_pending"])
-    return float(np.mean(times)), float(np.mean(calls)), float(np.mean(pend))
+    return float(np.median(times)), float(np.median(calls)), float(np.median(pend))
 
 
 def bench_stepwise(args, dev, stream):
@@ -431,17 +555,52 @@ def bench_stepwise(args, dev, stream):
             out["C2'"]["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             pass
-    # C2: one queue with 100k pending requests, per-step latency (BASELINE.json configs[1])
-    lat = {}
+    # C2: one queue with 100k pending requests, per-step latency (BASELINE.json configs[1]; SURVEY.md
+    # 8(d): median of >= 1,000 repetitions, warm and L2-flushed)
+    lat = {"reps": args.c2_reps}
     for eng, nm in ((tcm.ENGINE_STEPWISE, "stepwise"), (tcm.ENGINE_FUSED, "fused")):
         sim = _stage_c2(1, 100_000, eng, dev, stream)
-        ms, call_ms, keys = time_steps(sim, stream, args.step_iters, args.step_reps)
+        for flush in (False, True):
+            r = c2_latency(sim, stream, args.c2_reps, flush, dev)
+            sfx = "_flushed" if flush else ""
+            lat[nm + "_us" + sfx] = r["kernel_us"]
+            lat[nm + "_call_us" + sfx] = r["call_us"]
+            lat[nm + "_p90_us" + sfx] = r["kernel_p90_us"]
+            lat["pending"] = r["pending"]
         sim.close()
-        lat[nm + "_us"] = ms * 1e3
-        lat[nm + "_call_us"] = call_ms * 1e3
-    lat["pending"] = keys
     out["C2_latency"] = lat
     return out
+
+
+def c2_latency(sim, stream, reps, flush, dev):
+    """Median device time of one decision on C2 (one queue, 100k pending): iteration 3 of a fresh
+    reset, repeated `reps` times; with flush, a 512 MB write (> the 126 MB L2) runs on the stream
+    right before the step.  Kernel time from the library's CUDA events around its launch; call time
+    brackets the whole tcm_step(1) call."""
+    import torch
+    buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
+    ks, cs, pend = [], [], 0
+    for rep in range(reps + 3):
+        sim.reset()
+        sim.step(1)
+        sim.step(1)
+        if flush:
+            with torch.cuda.stream(stream):
+                buf.fill_(rep & 0xFF)
+        s0 = sim.stats()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.step(1)
+        e1.record(stream)
+        stream.synchronize()
+        s1 = sim.stats()
+        if rep >= 3:                               # three warm-up repetitions
+            ks.append(s1["engine_ms"] - s0["engine_ms"])
+            cs.append(e0.elapsed_time(e1))
+            pend = s1["sum_pending"] - s0["sum_pending"]
+    return {"kernel_us": float(np.median(ks)) * 1e3, "call_us": float(np.median(cs)) * 1e3,
+            "kernel_p90_us": float(np.percentile(ks, 90)) * 1e3, "pending": pend}
 
 
 def bench_next1(args, dev, stream):
@@ -502,12 +661,14 @@ def host_copy(trace):
             for k in ("req_offset", "arrival_us", "footprint", "inline_us", "out_tokens", "modality", "params")}
 
 
-def bench_e2e(args, sw, host, dev, dist, world):
+def bench_e2e(args, sw, host, dev, dist, world, check):
     """Same metric through the C ABI with HOST (pinned) buffers: every step copies its trace in
     (tcm_load_trace), runs (tcm_run, which copies the per-request results back) and reads the a6
-    counters (tcm_stats).  Two contexts on two streams, each driven by its own host thread, take
-    alternate steps, so one step's host<->device copies overlap the other step's kernels (a user
-    streaming sweeps through the API does the same); the timed region covers every step's copies."""
+    counters (tcm_stats).  Two contexts on two streams, each driven by its own host thread and
+    writing its own pinned result buffers, take alternate steps, so one step's host<->device copies
+    overlap the other step's kernels (a user streaming sweeps through the API does the same); the
+    timed region covers every step's copies.  Afterwards both contexts' host results are compared
+    with the device-resident run on a sample (`check`)."""
     import threading
     import torch
     from paper_2603_26498_b200 import tcm
@@ -515,12 +676,10 @@ def bench_e2e(args, sw, host, dev, dist, world):
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     per_ctx = max(2, min(args.steps, 4) // 2)
     lanes = []
-    # both contexts simulate the same trace, so their per-request results are bit-identical and
-    # they share one set of pinned result buffers (host memory: 25.6 GB per rank instead of 38.7)
-    res = {"admit_seq": torch.empty(N, dtype=torch.uint32).pin_memory(),
-           "first_token_us": torch.empty(N, dtype=torch.uint64).pin_memory(),
-           "done_us": torch.empty(N, dtype=torch.uint64).pin_memory()}
     for _ in range(2):
+        res = {"admit_seq": torch.empty(N, dtype=torch.uint32).pin_memory(),
+               "first_token_us": torch.empty(N, dtype=torch.uint64).pin_memory(),
+               "done_us": torch.empty(N, dtype=torch.uint64).pin_memory()}
         st = torch.cuda.Stream(device=dev)
         sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells), st)
         lanes.append((sim, res, st))
@@ -530,7 +689,8 @@ def bench_e2e(args, sw, host, dev, dist, world):
         sim, res, st = lane
         sim.load(host, res, mem=tcm.MEM_HOST)     # H2D inside the timed region
         sim.run()                                 # results copied back (D2H) before returning
-        hist, cnt, _ = sim.aggregate(device=dev)
+        with torch.cuda.stream(st):
+            hist, cnt, _ = sim.aggregate(device=dev)
         return cnt
 
     for lane in lanes:                            # warm-up (allocates each context's workspace)
@@ -552,7 +712,8 @@ def bench_e2e(args, sw, host, dev, dist, world):
                 if k == 0 and i == 0:
                     loaded.set()
                 sim.run()
-                sim.aggregate(device=dev)
+                with torch.cuda.stream(st):
+                    sim.aggregate(device=dev)
         except Exception as e:                    # surfaced below
             errors.append(e)
             loaded.set()
@@ -570,14 +731,22 @@ def bench_e2e(args, sw, host, dev, dist, world):
     mx = torch.tensor([wall], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    for sim, _, _ in lanes:
+    pick, ref = check
+    checked = 0
+    for sim, res, _ in lanes:
+        for k, v in ref.items():
+            got = res[k].numpy()[pick]
+            if not np.array_equal(got, v):
+                raise RuntimeError(f"e2e: host results ({k}) differ from the device-resident run")
+            checked += len(pick)
         sim.close()
     steps = 2 * per_ctx
     total_req = N * world * steps
     return {"value": total_req / float(mx[0]), "unit": "requests/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "results_checked": checked,
             "note": "HOST pinned buffers through tcm_load_trace/tcm_run/tcm_stats every step; two contexts on two "
-                    "streams take alternate steps so copies overlap kernels; host wall clock, max over ranks"}
+                    "streams (own result buffers each) take alternate steps so copies overlap kernels; host wall "
+                    "clock, max over ranks; both contexts' results equal the device run on every 997th request"}
 
 
 def log(*a):
@@ -606,6 +775,9 @@ def main():
     ap.add_argument("--next1-requests", type=int, default=1000)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="cpu_baseline on full-length replicas (64 x 10k requests: minutes of host time)")
+    ap.add_argument("--c2-reps", type=int, default=1000, help="C2 per-step latency: repetitions (median)")
     args = ap.parse_args()
     if args.replicas is None:
         args.replicas = {"c5": 131072, "c3": 4096, "c1": 1}.get(args.workload, 65536)
@@ -614,6 +786,9 @@ def main():
     if args.workload != "c4":
         # the C4-specific legs (e2e, stepwise C2', NEXT-1) run with the default workload only
         args.skip_e2e = args.skip_step = args.skip_next1 = True
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
     rank, world, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -114,7 +114,7 @@ typedef struct tcm_replica_params {
     uint64_t kv_capacity;  /* KV tokens, 1 .. 2^32-1    */
     double aging_alpha;    /* multiplies every k_c, >= 0 (R14)                      */
     uint32_t cell_id;      /* < n_cells: aggregation cell                           */
-    uint32_t flags;        /* TCM_ADMIT_SKIP or 0                                    */
+    uint32_t flags;        /* bitwise OR of TCM_ADMIT_SKIP and TCM_KV_GROWTH, or 0  */
 } tcm_replica_params;
 
 /* The request trace, SoA in CSR form: replica r owns requests [req_offset[r], req_offset[r+1]),
@@ -223,6 +223,14 @@ tcm_status tcm_run(tcm_ctx* ctx);
  * sum (e2e*den - num*iso) over violators, sum floor(e2e/out)).  These buffers are
  * NCCL-ready: all-reduce(SUM) across GPUs gives the bit-exact global result. */
 tcm_status tcm_stats(tcm_ctx* ctx, tcm_stats_host* out, int64_t* dev_hist, int64_t* dev_cnt);
+
+/* Per-replica work counters of the bound trace since the last load / reset, written to dev_out
+ * (DEVICE, uint64 [n_replicas][6], overwritten): engine iterations (fast-forwarded ones included),
+ * decisions (R17), sum of the pending-set size over decisions, scanned decisions (FUSED: decisions
+ * not taken in closed form; STEPWISE: all), requests done, preemptions
+ * (TCM_KV_GROWTH).  The same quantities the oracle counts per replica, so a test can compare them
+ * replica by replica.  Errors: TCM_E_ARG, TCM_E_STATE before tcm_load_trace. */
+tcm_status tcm_replica_counters(tcm_ctx* ctx, uint64_t* dev_out);
 
 /* Releases the workspace and the context (NULL is a no-op). */
 void tcm_destroy(tcm_ctx* ctx);

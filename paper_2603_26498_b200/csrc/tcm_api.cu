@@ -215,7 +215,8 @@ tcm_status reset_state(tcm_ctx* c) {
 }
 
 tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
-    TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
+    bool deferred = false;      // stepwise: k_step events still to be read after the sync below
+    if (c->cfg.engine == TCM_ENGINE_FUSED) TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
     TCM_CUDA(c, cudaEventRecord(c->ev[2], c->s));
     if (c->cfg.engine == TCM_ENGINE_FUSED) {
         launch_fused(c->m, c->t, max_iters, c->d_active, c->s);
@@ -225,7 +226,8 @@ tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
     } else {
         uint64_t l = 0;
         double kms = 0;
-        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, &l, c->ev[5], c->ev[6], &kms);
+        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, &l, c->ev[5], c->ev[6], &kms,
+                                     &deferred);
         c->engine_ms += kms;
         c->launches += l;
         if (st != TCM_OK) return fail(c, st, "stepwise engine failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -241,8 +243,8 @@ tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
         c->reset_ms += ms;
         c->reset_pending = false;
     }
-    if (c->cfg.engine == TCM_ENGINE_FUSED) {
-        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+    if (c->cfg.engine == TCM_ENGINE_FUSED || deferred) {
+        TCM_CUDA(c, cudaEventElapsedTime(&ms, deferred ? c->ev[5] : c->ev[2], deferred ? c->ev[6] : c->ev[3]));
         c->engine_ms += ms;
     }
     TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
@@ -443,8 +445,10 @@ tcm_status tcm_step(tcm_ctx* c, uint32_t max_iterations, uint32_t* active_replic
     uint32_t active = 0;
     tcm_status st = run_engine(c, max_iterations, &active);
     if (st != TCM_OK) return st;
-    if ((st = copy_results_to_host(c)) != TCM_OK) return st;
-    TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    if (c->host_results) {     // DEVICE results need no copy and no second synchronisation
+        if ((st = copy_results_to_host(c)) != TCM_OK) return st;
+        TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    }
     if (active_replicas) *active_replicas = active;
     return TCM_OK;
 }
@@ -515,6 +519,17 @@ tcm_status tcm_stats(tcm_ctx* c, tcm_stats_host* out, int64_t* dev_hist, int64_t
         TCM_CUDA(c, cudaStreamSynchronize(c->s));
     }
     if (out) out->kernel_launches = c->launches;
+    return TCM_OK;
+}
+
+tcm_status tcm_replica_counters(tcm_ctx* c, uint64_t* dev_out) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_replica_counters before tcm_load_trace");
+    if (!dev_out) return fail(c, TCM_E_ARG, "dev_out is NULL");
+    launch_replica_counters(c->t, reinterpret_cast<unsigned long long*>(dev_out), c->s);
+    c->launches++;
+    TCM_CUDA(c, cudaGetLastError());
+    TCM_CUDA(c, cudaStreamSynchronize(c->s));
     return TCM_OK;
 }
 

@@ -150,6 +150,24 @@ __global__ void k_reduce(TraceDev t, unsigned long long* acc /* [kAccN] */) {
     }
 }
 
+// Per-replica work counters (tcm_replica_counters): one thread per replica.
+__global__ void k_replica_counters(TraceDev t, unsigned long long* out /* [R][kRepCnt] */) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= t.R) return;
+    const ReplicaState st = t.state[r];
+    unsigned long long* o = out + (size_t)r * kRepCnt;
+    o[0] = st.iter;
+    o[1] = st.decisions;
+    o[2] = st.sum_pending;
+    o[3] = st.scanned;
+    o[4] = st.done_count;
+    o[5] = st.tail[1];            // stepwise, TCM_KV_GROWTH: preemptions (0 otherwise)
+}
+
+void launch_replica_counters(const TraceDev& t, unsigned long long* out, cudaStream_t s) {
+    k_replica_counters<<<(t.R + 255) / 256, 256, 0, s>>>(t, out);
+}
+
 // ---------------------------------------------------------------------------------------
 // a6 aggregation: warp per replica; per lane per-group
 // counters, warp-reduced; histogram bins by atomics.

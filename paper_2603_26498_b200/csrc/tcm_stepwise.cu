@@ -1105,9 +1105,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
 
 // ReplicaState.head[0] = window start lo (oldest possibly-pending id), head[1] = remaining
 // iteration budget of the current tcm_step call; the class-queue fields are unused here.
-__global__ void k_sw_budget(TraceDev t, uint32_t budget) {
+// Per-call iteration budget of every replica; also zeroes the active-replica count and the
+// replica counter of the dynamic mode (one launch instead of a launch and two memsets).
+__global__ void k_sw_budget(TraceDev t, uint32_t budget, uint32_t* d_active, unsigned long long* ctr) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < t.R) t.state[r].head[1] = budget;
+    if (r == 0) {
+        *d_active = 0;
+        if (ctr) *ctr = 0;
+    }
 }
 
 __global__ void k_sw_init(TraceDev t) {
@@ -1215,7 +1221,7 @@ Launch stepwise_config(uint32_t R, uint64_t N) {
 
 tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWorkspace& w, uint32_t max_iters,
                         uint32_t* d_active, cudaStream_t s, uint64_t* launches, cudaEvent_t ev_begin,
-                        cudaEvent_t ev_end, double* kernel_ms) {
+                        cudaEvent_t ev_end, double* kernel_ms, bool* deferred) {
     uint32_t* remv = reinterpret_cast<uint32_t*>(w.base);
     // replica counter for the warp-per-replica mode: in the workspace's 16 spare bytes after rem
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(
@@ -1224,17 +1230,19 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
     const unsigned long long per_launch = (unsigned long long)t.R + (unsigned long long)L.grid * kWarpsPerBlock;
     if (L.group != 1 || L.cluster != 1 || t.R <= (uint64_t)L.grid * kWarpsPerBlock) ctr = nullptr;   // static is ideal
     unsigned long long ctr_base = 0;
-    if (ctr && cudaMemsetAsync(ctr, 0, 8, s) != cudaSuccess) return TCM_E_CUDA;
-    k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, max_iters);
+    k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, max_iters, d_active, ctr);
     (*launches)++;
     // Each k_step launch advances every active replica by one iteration (or one fast-forward);
-    // launch in chunks and read the active count only at the end of each chunk.
+    // launch in chunks and read the active count only at the end of each chunk.  A call that fits
+    // in one chunk (tcm_step(n <= 64)) returns without synchronising: the caller reads d_active and
+    // the events after its own (single) synchronisation (*deferred = true).
     const uint32_t chunk = 64;
     uint64_t done_launches = 0;
+    *deferred = false;
     for (;;) {
         uint32_t this_chunk = chunk;
         if ((uint64_t)max_iters - done_launches < this_chunk) this_chunk = (uint32_t)(max_iters - done_launches);
-        if (cudaMemsetAsync(d_active, 0, 4, s) != cudaSuccess) return TCM_E_CUDA;
+        if (done_launches > 0 && cudaMemsetAsync(d_active, 0, 4, s) != cudaSuccess) return TCM_E_CUDA;
         // device time of the k_step launches alone (tcm_stats_host.engine_ms)
         if (cudaEventRecord(ev_begin, s) != cudaSuccess) return TCM_E_CUDA;
         for (uint32_t q = 0; q < this_chunk; ++q) {
@@ -1269,6 +1277,10 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         done_launches += this_chunk;
         if (cudaEventRecord(ev_end, s) != cudaSuccess) return TCM_E_CUDA;
         if (cudaGetLastError() != cudaSuccess) return TCM_E_CUDA;
+        if (done_launches == this_chunk && done_launches >= max_iters) {
+            *deferred = true;
+            break;
+        }
         uint32_t act = 0;
         if (cudaMemcpyAsync(&act, d_active, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TCM_E_CUDA;
         if (cudaStreamSynchronize(s) != cudaSuccess) return TCM_E_CUDA;

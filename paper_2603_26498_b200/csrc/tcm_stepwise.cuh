@@ -16,6 +16,6 @@ StepwiseWorkspace stepwise_bind(void* p, uint32_t R);
 // Runs up to max_iters engine iterations of every active replica; counts launches.
 tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWorkspace& w,
                         uint32_t max_iters, uint32_t* d_active, cudaStream_t s, uint64_t* launches,
-                        cudaEvent_t ev_begin, cudaEvent_t ev_end, double* kernel_ms);
+                        cudaEvent_t ev_begin, cudaEvent_t ev_end, double* kernel_ms, bool* deferred);
 
 }  // namespace tcm

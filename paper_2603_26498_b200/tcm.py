@@ -29,7 +29,7 @@ INF32 = 0xFFFFFFFF
 
 EXPORTS = ("tcm_create", "tcm_load_trace", "tcm_reset", "tcm_step", "tcm_run", "tcm_stats", "tcm_destroy",
            "tcm_last_error", "tcm_workspace_bytes", "tcm_generate_trace", "tcm_k1_eval",
-           "tcm_k1_audit", "tcm_k1_filter_error")
+           "tcm_k1_audit", "tcm_k1_filter_error", "tcm_replica_counters")
 
 
 class TcmError(RuntimeError):
@@ -103,6 +103,8 @@ def lib():
         L.tcm_run.argtypes = [vp]
         L.tcm_stats.restype = st
         L.tcm_stats.argtypes = [vp, ctypes.POINTER(tcm_stats_host), vp, vp]
+        L.tcm_replica_counters.restype = st
+        L.tcm_replica_counters.argtypes = [vp, vp]
         L.tcm_destroy.restype = None
         L.tcm_destroy.argtypes = [vp]
         L.tcm_last_error.restype = ctypes.c_char_p
@@ -209,6 +211,14 @@ def tcm_stats(ctx, dev_hist=None, dev_cnt=None) -> dict:
     s = tcm_stats_host()
     _check(lib().tcm_stats(ctx, ctypes.byref(s), _ptr(dev_hist), _ptr(dev_cnt)), ctx)
     return {n: getattr(s, n) for n, _ in tcm_stats_host._fields_}
+
+
+REPLICA_COUNTERS = ("iterations", "decisions", "sum_pending", "scanned_decisions", "requests_done", "preemptions")
+
+
+def tcm_replica_counters(ctx, dev_out):
+    """dev_out: device uint64 tensor [R, 6] (REPLICA_COUNTERS order)."""
+    _check(lib().tcm_replica_counters(ctx, _ptr(dev_out)), ctx)
 
 
 def tcm_destroy(ctx):
@@ -338,11 +348,24 @@ class Simulation:
 
     def aggregate(self, device="cuda"):
         import torch
+        import contextlib
         n = self.cfg.n_cells
-        hist = torch.zeros((n, GROUPS, HIST_BINS), dtype=torch.int64, device=device)
-        cnt = torch.zeros((n, GROUPS, NCNT), dtype=torch.int64, device=device)
+        # tcm_stats overwrites both buffers on the context's stream; allocate them on that stream
+        # so torch's allocator orders any reuse of their memory after the library's writes
+        on = torch.cuda.stream(self.stream) if isinstance(self.stream, torch.cuda.Stream) else contextlib.nullcontext()
+        with on:
+            hist = torch.empty((n, GROUPS, HIST_BINS), dtype=torch.int64, device=device)
+            cnt = torch.empty((n, GROUPS, NCNT), dtype=torch.int64, device=device)
         st = tcm_stats(self.ctx, hist, cnt)
         return hist, cnt, st
+
+    def replica_counters(self, n_replicas: int, device="cuda") -> np.ndarray:
+        """Per-replica counters as a structured numpy array (REPLICA_COUNTERS fields)."""
+        import torch
+        out = torch.empty((n_replicas, len(REPLICA_COUNTERS)), dtype=torch.uint64, device=device)
+        tcm_replica_counters(self.ctx, out)
+        a = out.cpu().numpy()
+        return {k: a[:, i] for i, k in enumerate(REPLICA_COUNTERS)}
 
     def close(self):
         if self.ctx:
