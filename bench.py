@@ -456,7 +456,10 @@ def run_tcm(args, rank, world, local):
         host = host_copy(trace)
         # a sample of the device-resident run's results: the e2e leg's outputs are checked against it
         pick = torch.arange(0, N, 997, device=dev)
-        ref = {k: results[k][pick].cpu().numpy() for k in ("admit_seq", "first_token_us", "done_us")}
+        def take(x):       # torch has no index kernels for unsigned dtypes: gather through a signed view
+            sig = {torch.uint32: (torch.int32, np.uint32), torch.uint64: (torch.int64, np.uint64)}.get(x.dtype)
+            return x[pick].cpu().numpy() if sig is None else x.view(sig[0])[pick].cpu().numpy().view(sig[1])
+        ref = {k: take(results[k]) for k in ("admit_seq", "first_token_us", "done_us")}
         sim.close()
         del trace, results
         torch.cuda.empty_cache()

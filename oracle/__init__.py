@@ -107,6 +107,9 @@ def lib():
         L.orc_simulate_growth.restype = i
         L.orc_simulate_growth.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32] + \
             [ctypes.c_void_p] * 14 + [u64]
+        L.orc_decide.restype = ctypes.c_int
+        L.orc_decide.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, u64, u64,
+                                 ctypes.c_uint32] + [ctypes.c_void_p] * 9
         L.orc_ttft_bucket.restype = ctypes.c_uint32
         L.orc_ttft_bucket.argtypes = [u64]
         L.orc_aggregate.restype = None
@@ -235,6 +238,32 @@ class GrowthResult:
     cls: np.ndarray
     counters: dict
     status: int
+
+
+def decide(arrival_us, footprint, inline_us, out_tokens, cls, rem, reserved, clock, kv_free, n_dec,
+           policy=TCM, alpha=1.0, chunk_budget=2048, m: OrcModel | None = None, admit_skip=False):
+    """One decision on an explicit state; every request is pending.
+    Returns (chunk per request, admit rank per request or -1, tokens, inline, kv_free after, Bp)."""
+    m = m or model()
+    n = len(arrival_us)
+    a = np.ascontiguousarray(arrival_us, dtype=np.uint64)
+    f = np.ascontiguousarray(footprint, dtype=np.uint32)
+    il = np.ascontiguousarray(inline_us, dtype=np.uint32)
+    o = np.ascontiguousarray(out_tokens, dtype=np.uint16)
+    cl = np.ascontiguousarray(cls, dtype=np.uint8)
+    rem0 = np.ascontiguousarray(rem, dtype=np.uint32)
+    rm = rem0.copy()
+    rs = np.ascontiguousarray(reserved, dtype=np.uint8).copy()
+    seq = np.full(n, 0xFFFFFFFF, dtype=np.uint32)
+    res = np.zeros(4, dtype=np.uint64)
+    r = OrcReplica(policy, chunk_budget, 1 << 40, alpha, int(admit_skip), 0)
+    st = lib().orc_decide(ctypes.byref(m), ctypes.byref(r), n, int(clock), int(kv_free), int(n_dec),
+                          a.ctypes.data, f.ctypes.data, il.ctypes.data, o.ctypes.data, cl.ctypes.data,
+                          rm.ctypes.data, rs.ctypes.data, seq.ctypes.data, res.ctypes.data)
+    if st != 0:
+        raise ValueError("orc_decide: bad argument")
+    adm = np.where(seq == 0xFFFFFFFF, -1, seq.astype(np.int64))
+    return (rem0 - rm).astype(np.int64), adm, int(res[0]), int(res[1]), int(res[2]), int(res[3])
 
 
 def simulate_growth(arrival_us, footprint, inline_us, out_tokens, modality, policy=TCM, alpha=1.0,

@@ -181,6 +181,102 @@ static int orc_cmp_age(const void* a, const void* b)
     return x->id < y->id ? -1 : (x->id > y->id);
 }
 
+/* One decision, over the pending ids `pending[0..n_pend)` (id order):
+ * 3 the budget left after decodes (R8); 4-5 key every pending request and sort (TCM), or take
+ * arrival order (FCFS); 6 the greedy admission scan, where the first KV misfit blocks later NEW
+ * admits but partials still get chunks (R5-R7).  Updates rem / reserved / kv_free / seq /
+ * admit_seq in place; returns Bp. */
+static uint32_t orc_admit_step(const orc_model* m, const orc_replica* r, const double* C, const int* zero,
+                               uint64_t clock, uint32_t n_dec, uint32_t n_pend, const uint32_t* pending,
+                               const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
+                               const uint16_t* out, const uint8_t* cls, uint32_t* rem, uint8_t* reserved,
+                               uint64_t* kv_free_io, uint32_t* seq_io, uint32_t* admit_seq,
+                               orc_entry* order, uint64_t* tok_out, uint64_t* inl_out,
+                               uint32_t* n_admitted)
+{
+    /* 3 budget left after decodes (R8) */
+    uint32_t Bp = r->chunk_budget > n_dec ? r->chunk_budget - n_dec : 0;
+
+    /* 4-5 key every pending request and sort (TCM), or arrival order (FCFS) */
+    for (uint32_t q = 0; q < n_pend; ++q) {
+        uint32_t i = pending[q];
+        order[q].id = i;
+        order[q].arrival = arrival[i];
+        order[q].P = 0.0;
+        order[q].dl = 0;
+        if (r->policy == ORC_TCM) {
+            int c = cls[i];
+            order[q].P = orc_priority(m->S[c], m->p[c], C[c], zero[c], clock - arrival[i]);
+        } else if (r->policy == ORC_EDF) {
+            order[q].dl = arrival[i] * m->slo_den +
+                          m->slo_num * orc_iso_e2e(m, r->chunk_budget, f[i], inl[i], out[i]);
+        } else if (r->policy == ORC_NAIVE_AGING) {
+            order[q].dl = clock - arrival[i];
+        }
+    }
+    if (r->policy == ORC_TCM) qsort(order, n_pend, sizeof(orc_entry), orc_cmp);
+    if (r->policy == ORC_EDF) qsort(order, n_pend, sizeof(orc_entry), orc_cmp_edf);
+    if (r->policy == ORC_NAIVE_AGING) qsort(order, n_pend, sizeof(orc_entry), orc_cmp_age);
+
+    /* 6 admission scan: greedy chunks; first KV misfit blocks later NEW admits (R6) */
+    uint64_t kv_free = *kv_free_io;
+    uint32_t seq = *seq_io;
+    uint32_t left = Bp;
+    int blocked = 0;
+    uint64_t tok = 0, inl_sum = 0;
+    for (uint32_t q = 0; q < n_pend; ++q) {
+        uint32_t i = order[q].id;
+        if (left == 0) break;
+        if (!reserved[i]) {
+            if (blocked) continue;
+            if ((uint64_t)f[i] > kv_free) { blocked = !r->admit_skip; continue; }
+            reserved[i] = 1;
+            kv_free -= f[i];
+            admit_seq[i] = seq++;
+            inl_sum += inl[i];
+            (*n_admitted)++;
+        }
+        uint32_t c = rem[i] < left ? rem[i] : left;
+        rem[i] -= c;
+        left -= c;
+        tok += c;
+    }
+    *kv_free_io = kv_free;
+    *seq_io = seq;
+    *tok_out = tok;
+    *inl_out = inl_sum;
+    return Bp;
+}
+
+/* One decision on an explicit state (test infrastructure: SURVEY.md 8(c) single-step brute force).
+ * Requests 0..n-1 are all pending, in id order; rem / reserved carry partial prefills in and the
+ * decision out; admit_seq[i] = the admission rank of a request admitted now, else unchanged.
+ * res[0] = tokens scheduled, res[1] = inline time charged, res[2] = kv_free after, res[3] = Bp. */
+int orc_decide(const orc_model* m, const orc_replica* r, uint32_t n, uint64_t clock, uint64_t kv_free,
+               uint32_t n_dec, const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
+               const uint16_t* out, const uint8_t* cls, uint32_t* rem, uint8_t* reserved,
+               uint32_t* admit_seq, uint64_t* res)
+{
+    if (r->chunk_budget == 0 || r->policy > ORC_NAIVE_AGING || r->admit_skip > 1) return -1;
+    double C[3];
+    int zero[3];
+    for (int c = 0; c < 3; ++c) C[c] = orc_k1_const(r->alpha, m->k[c], m->p[c], &zero[c]);
+    uint32_t* pending = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1));
+    orc_entry* order = (orc_entry*)malloc(sizeof(orc_entry) * (n + 1));
+    if (!pending || !order) { free(pending); free(order); return -1; }
+    for (uint32_t i = 0; i < n; ++i) pending[i] = i;
+    uint32_t seq = 0, nadm = 0;
+    uint64_t tok = 0, inl_sum = 0;
+    uint32_t Bp = orc_admit_step(m, r, C, zero, clock, n_dec, n, pending, arrival, f, inl, out, cls, rem,
+                                 reserved, &kv_free, &seq, admit_seq, order, &tok, &inl_sum, &nadm);
+    res[0] = tok;
+    res[1] = inl_sum;
+    res[2] = kv_free;
+    res[3] = Bp;
+    free(pending); free(order);
+    return 0;
+}
+
 int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
                  const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
                  const uint16_t* out, const uint8_t* mod, uint32_t* admit_seq,
@@ -239,52 +335,12 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
         rec.n_pending = n_pend;
         rec.n_dec = n_dec;
 
-        /* 3 budget left after decodes (R8) */
-        uint32_t Bp = r->chunk_budget > n_dec ? r->chunk_budget - n_dec : 0;
-        rec.budget = Bp;
-
-        /* 4-5 key every pending request and sort (TCM), or arrival order (FCFS) */
-        for (uint32_t q = 0; q < n_pend; ++q) {
-            uint32_t i = pending[q];
-            order[q].id = i;
-            order[q].arrival = arrival[i];
-            order[q].P = 0.0;
-            order[q].dl = 0;
-            if (r->policy == ORC_TCM) {
-                int c = cls_out[i];
-                order[q].P = orc_priority(m->S[c], m->p[c], C[c], zero[c], clock - arrival[i]);
-            } else if (r->policy == ORC_EDF) {
-                order[q].dl = arrival[i] * m->slo_den +
-                              m->slo_num * orc_iso_e2e(m, r->chunk_budget, f[i], inl[i], out[i]);
-            } else if (r->policy == ORC_NAIVE_AGING) {
-                order[q].dl = clock - arrival[i];
-            }
-        }
-        if (r->policy == ORC_TCM) qsort(order, n_pend, sizeof(orc_entry), orc_cmp);
-        if (r->policy == ORC_EDF) qsort(order, n_pend, sizeof(orc_entry), orc_cmp_edf);
-        if (r->policy == ORC_NAIVE_AGING) qsort(order, n_pend, sizeof(orc_entry), orc_cmp_age);
-
-        /* 6 admission scan: greedy chunks; first KV misfit blocks later NEW admits (R6) */
-        uint32_t left = Bp;
-        int blocked = 0;
+        /* 3-6 budget, keys, order, admission scan (one decision) */
         uint64_t tok = 0, inl_sum = 0;
-        for (uint32_t q = 0; q < n_pend; ++q) {
-            uint32_t i = order[q].id;
-            if (left == 0) break;
-            if (!reserved[i]) {
-                if (blocked) continue;
-                if ((uint64_t)f[i] > kv_free) { blocked = !r->admit_skip; continue; }
-                reserved[i] = 1;
-                kv_free -= f[i];
-                admit_seq[i] = seq++;
-                inl_sum += inl[i];
-                rec.n_admitted++;
-            }
-            uint32_t c = rem[i] < left ? rem[i] : left;
-            rem[i] -= c;
-            left -= c;
-            tok += c;
-        }
+        uint32_t Bp = orc_admit_step(m, r, C, zero, clock, n_dec, n_pend, pending, arrival, f, inl, out,
+                                     cls_out, rem, reserved, &kv_free, &seq, admit_seq, order,
+                                     &tok, &inl_sum, &rec.n_admitted);
+        rec.budget = Bp;
         rec.kv_free_admit = kv_free;
         rec.tokens = (uint32_t)tok;
 

@@ -109,6 +109,20 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
                  uint64_t max_iters);
 
 /*
+ * One decision on an explicit state: requests 0..n-1 are all pending,
+ * in id order, with their class, remaining prefill `rem` and reserved (partial) flag; the engine
+ * has n_dec decoding sequences and kv_free free KV at `clock`.  This is the same code the engine
+ * loop above runs for each decision.  On return rem / reserved hold the decision, admit_seq[i]
+ * is the admission rank (0, 1, ...) of each request admitted now (others untouched), and
+ * res = {tokens, inline_us charged, kv_free after, budget Bp}.  Returns 0 or -1 (bad argument).
+ * Test infrastructure for the single-step brute force.
+ */
+int orc_decide(const orc_model* m, const orc_replica* r, uint32_t n, uint64_t clock, uint64_t kv_free,
+               uint32_t n_dec, const uint64_t* arrival_us, const uint32_t* footprint,
+               const uint32_t* inline_us, const uint16_t* out_tokens, const uint8_t* cls,
+               uint32_t* rem, uint8_t* reserved, uint32_t* admit_seq, uint64_t* res);
+
+/*
  * NEXT-1: the same engine loop with decode KV growth and preemption by
  * recomputation, readings R28-R32.  A running request holds its reservation plus
  * one KV token per decode iteration run.  At the start of every iteration, while

@@ -63,3 +63,35 @@ def test_summary_examples():
     hist, cnt = O.aggregate(tr2, fake, m=m)
     assert cnt[3, 3] == 1
     assert cnt[3, 4] == 10_000_000 * 557_500 - 4_000_000 * 557_500   # severity 6 s x den
+
+
+def _check_golden(case, policy):
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "histogram.json")))[case]
+    tr = T.from_requests(g["requests"])
+    r = O.simulate(tr.arrival_us, tr.footprint, tr.inline_us, tr.out_tokens, tr.modality, policy=policy)
+    assert r.status == 0
+    hist, cnt = O.aggregate(tr, r)
+    col = {"n": 0, "sum_ttft": 1, "sum_e2e": 2, "viol": 3, "severity": 4, "sum_norm": 5}
+    for gname, exp in g["expect"].items():
+        gi = {"M": 0, "C": 1, "T": 2, "All": 3}[gname]
+        for k, v in exp.items():
+            if k == "bins":
+                nz = {str(b): int(hist[gi, b]) for b in np.nonzero(hist[gi])[0]}
+                assert nz == v, (case, gname)
+            elif k == "rate":
+                assert cnt[gi, 3] / cnt[gi, 0] == v
+            else:
+                assert cnt[gi, col[k]] == v, (case, gname, k)
+
+
+def test_hand_worked_histogram_isolated_requests():
+    # tests/golden/histogram.json: SPEC.md:147-149 isolated requests, buckets derived by hand
+    _check_golden("isolated_three", O.FCFS)
+    _check_golden("isolated_three", O.TCM)
+
+
+def test_hand_worked_violation_rates():
+    # SPEC.md:523 overall rate 0.25 from class rates 0.5 (n=2) and 0.0 (n=2), via SURVEY H1 under FCFS
+    _check_golden("violation_rates", O.FCFS)

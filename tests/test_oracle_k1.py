@@ -149,3 +149,79 @@ def test_monotone_in_waiting_time(c, lo, hi):
 def test_monotone_alpha_grid(alpha):
     for c in range(3):
         assert O.audit_monotone(c, 0, 400_000, alpha=alpha) is None
+
+
+# ---------------------------------------------------------------------------------------------
+# 10^6-sample pins (SURVEY.md 8(c) "K1" row) against an independent extended-precision evaluation:
+# numpy's long double (x87 80-bit, 64-bit significand: 11 bits more than binary64) through libm's
+# logl / expl / powl.  Stage by stage, then the whole key against the paper's formula.
+# (A final-P bound of 4 ulp is not attainable by ANY binary64 evaluation through ln(w in us):
+# 0.5 ulp of L ~ 20 is 1.8e-15 absolute, times p = 3.5 -- see DESIGN.md reading R33.)
+import numpy as np
+
+_LD = np.longdouble
+_N6 = 1_000_000
+
+
+def _ulp(x):
+    return np.spacing(np.abs(np.asarray(x, dtype=np.float64))).astype(_LD)
+
+
+def test_ln_million_samples_within_1_5_ulp():
+    L = O.lib()
+    rng = np.random.default_rng(61)
+    v = np.ldexp(1 + rng.random(_N6), rng.integers(-60, 61, _N6))
+    got = np.fromiter((L.orc_ln(float(x)) for x in v), np.float64, _N6).astype(_LD)
+    ref = np.log(v.astype(_LD))
+    # absolute error in ulps of max(|ln v|, 1): LN.5's table + series sum is absolute-accurate
+    err = np.abs(got - ref) / _ulp(np.maximum(np.abs(ref), 1))
+    assert float(err.max()) <= 1.5, float(err.max())
+
+
+def test_exp_million_samples_within_6_ulp():
+    L = O.lib()
+    rng = np.random.default_rng(62)
+    y = rng.uniform(-740.0, 700.0, _N6)
+    got = np.fromiter((L.orc_exp(float(x)) for x in y), np.float64, _N6)
+    ref = np.exp(y.astype(_LD))
+    ok = got >= 2.0**-1022                        # EXP.7 flushes the subnormal range by spec
+    assert np.all(ref[~ok] < _LD(2.0**-1021))
+    err = np.abs(got[ok].astype(_LD) - ref[ok]) / _ulp(got[ok])
+    # T[j] 0.5 ulp + degree-6 Taylor truncation r^7/7! <= 2 ulp on |r| <= ln2/32 + 3 roundings
+    assert float(err.max()) <= 6.0, float(err.max())
+    assert float(np.median(err.astype(np.float64))) <= 1.0
+
+
+def test_priority_million_samples_vs_paper_formula():
+    # PAPER.md:457 with PAPER.md:580 constants, w in seconds (R1), alpha on the sweep grid (R14):
+    # P_ref = S + (1 - exp(-alpha k (w/1e6)^p)) in long double.  Bound: every stage of K1 within
+    # 4 ulp of its exact result, propagated forward (dP = e x dy): dL, dC -> dy -> dx/x -> de.
+    L = O.lib()
+    rng = np.random.default_rng(63)
+    alphas = np.array([0.0] + [2.0**e for e in range(-7, 8)])
+    c = rng.integers(0, 3, _N6)
+    a = alphas[rng.integers(0, len(alphas), _N6)]
+    w = np.floor(10 ** rng.uniform(0, 10.5, _N6)).astype(np.uint64)
+    Sv, Kv, Pv = np.array(S)[c], np.array(K)[c], np.array(P)[c]
+    consts = {}
+    got = np.empty(_N6)
+    for i in range(_N6):
+        key = (int(c[i]), float(a[i]))
+        if key not in consts:
+            consts[key] = O.k1_const(a[i], Kv[i], Pv[i])
+        C, z = consts[key]
+        got[i] = L.orc_priority(Sv[i], Pv[i], C, z, int(w[i]))
+    wl = w.astype(_LD) / _LD(10**6)
+    x = (a.astype(_LD) * Kv.astype(_LD)) * wl ** Pv.astype(_LD)
+    e = np.exp(-x)
+    ref = Sv.astype(_LD) + (_LD(1) - e)
+    ref = np.where((w == 0) | (a == 0), Sv.astype(_LD), ref)
+    lnw = np.log(np.maximum(w, 1).astype(_LD))
+    yv = np.where(x > 0, np.log(np.where(x > 0, x, _LD(1))), _LD(0))
+    dy = 4 * (Pv * _ulp(np.maximum(lnw, 1)) + _ulp(np.maximum(np.abs(yv), 1))
+              + Pv * _ulp(np.log(1e6)) + _ulp(np.maximum(np.abs(np.log(np.maximum(a * Kv, 1e-300))), 1)))
+    de = e * x * (dy + 4 * _LD(2.0**-52)) + 4 * _ulp(e)
+    bound = de + 2 * _ulp(ref)
+    err = np.abs(got.astype(_LD) - ref)
+    assert np.all(err <= bound), float(np.max(err / bound))
+    assert float(err.max()) < 5e-15                    # the absolute budget of the 3,000-sample pin
