@@ -632,18 +632,13 @@ def bench_next1(args, dev, stream):
         times.append(e0.elapsed_time(e1))
     st = sim.stats()
     ms = times[-1]
-    # per policy and class (R13 smart thresholds): fig:preemptions
+    # per policy and class (the engine's a1 classifier, on the device): fig:preemptions
     from paper_2603_26498_b200 import metrics as M
-    pc = res["preempt_count"].cpu().numpy()
-    pt = res["preempted_us"].cpu().numpy()
-    fp = tr["footprint"].cpu().numpy()
-    md = tr["modality"].cpu().numpy()
-    off = tr["req_offset"].cpu().numpy().astype(np.int64)
-    pol = np.repeat(sw.params["policy"], np.diff(off))
+    pst = sim.preemption_stats(device=dev).cpu().numpy()          # [cells][M, C, T, all][3]
+    cell_pol = np.array([c["policy"] for c in sw.cells])
     by = {}
     for name, p in (("FCFS", tcm.POLICY_FCFS), ("TCM", tcm.POLICY_TCM)):
-        sel = pol == p
-        summ = M.preemption_summary(md[sel], fp[sel], pc[sel], pt[sel])
+        summ = M.preemption_summary(pst[cell_pol == p])
         by[name] = {"preemptions": summ["all"]["preemptions"], "motorcycle_preemptions": summ["M"]["preemptions"],
                     "requests_preempted": summ["all"]["requests_preempted"],
                     "preempted_s": {g: round(summ[g]["preempted_s"], 3) for g in ("M", "C", "T")}}

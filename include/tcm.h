@@ -232,6 +232,13 @@ tcm_status tcm_stats(tcm_ctx* ctx, tcm_stats_host* out, int64_t* dev_hist, int64
  * replica by replica.  Errors: TCM_E_ARG, TCM_E_STATE before tcm_load_trace. */
 tcm_status tcm_replica_counters(tcm_ctx* ctx, uint64_t* dev_out);
 
+/* fig:preemptions per (cell, group): dev_out (DEVICE, int64
+ * [n_cells][4][3], overwritten; groups M, C, T, all by the engine's own a1 classifier) = number of
+ * preemptions, total preempted time (us, R31) and number of requests preempted at least once, over
+ * the per-request NEXT-1 results of the bound trace (replicas without TCM_KV_GROWTH add zeros).
+ * Errors: TCM_E_ARG, TCM_E_STATE before tcm_load_trace. */
+tcm_status tcm_preemption_stats(tcm_ctx* ctx, int64_t* dev_out);
+
 /* Releases the workspace and the context (NULL is a no-op). */
 void tcm_destroy(tcm_ctx* ctx);
 

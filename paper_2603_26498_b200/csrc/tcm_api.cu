@@ -533,6 +533,20 @@ tcm_status tcm_replica_counters(tcm_ctx* c, uint64_t* dev_out) {
     return TCM_OK;
 }
 
+tcm_status tcm_preemption_stats(tcm_ctx* c, int64_t* dev_out) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_preemption_stats before tcm_load_trace");
+    if (!dev_out) return fail(c, TCM_E_ARG, "dev_out is NULL");
+    TCM_CUDA(c, cudaMemsetAsync(dev_out, 0, (size_t)c->m.n_cells * kGroups * 3 * 8, c->s));
+    if (c->t.pcount) {                  // NEXT-1 results exist (some replica runs TCM_KV_GROWTH)
+        launch_preempt_stats(c->m, c->t, reinterpret_cast<unsigned long long*>(dev_out), c->s);
+        c->launches++;
+        TCM_CUDA(c, cudaGetLastError());
+    }
+    TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    return TCM_OK;
+}
+
 void tcm_destroy(tcm_ctx* c) {
     if (!c) return;
     free_allocs(c);

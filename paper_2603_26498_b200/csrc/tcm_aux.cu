@@ -22,7 +22,7 @@ __global__ void k_init(TraceDev t) {
     st.n_pend = 0;
     for (int c = 0; c < 3; ++c) {
         st.head[c] = NIL;
-        st.tail[c] = NIL;
+        st.tail[c] = 0;      // stepwise NEXT-1 counters (tcm_stats preemptions); unused by the fused engine
         st.rem[c] = 0;
     }
     st.flags = 0;
@@ -162,6 +162,48 @@ __global__ void k_replica_counters(TraceDev t, unsigned long long* out /* [R][kR
     o[3] = st.scanned;
     o[4] = st.done_count;
     o[5] = st.tail[1];            // stepwise, TCM_KV_GROWTH: preemptions (0 otherwise)
+}
+
+// fig:preemptions per (cell, group): warp per replica, lanes over its requests; the class is the
+// engine's own a1 classifier (classify(), R13); warp-reduced, one atomic per counter and replica.
+__global__ void k_preempt_stats(ModelConst m, TraceDev t, unsigned long long* out /* [cells][4][3] */) {
+    const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (r >= t.R) return;
+    const uint64_t a = t.offset[r], b = t.offset[r + 1];
+    unsigned long long v[kGroups - 1][3] = {};
+    for (uint64_t i = a + lane; i < b; i += 32) {
+        const uint32_t pc = t.pcount[i];
+        if (pc == 0) continue;
+        const int g = classify(m, t.mod[i], t.footprint[i]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (c == g) {
+                v[c][0] += pc;
+                v[c][1] += t.ptime[i];
+                v[c][2] += 1;
+            }
+        }
+    }
+    unsigned long long* o = out + (size_t)t.params[r].cell_id * kGroups * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            unsigned long long x = v[c][k];
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, s);
+            if (lane == 0 && x) {
+                atomicAdd(o + c * 3 + k, x);
+                atomicAdd(o + 3 * 3 + k, x);          // group "all"
+            }
+        }
+    }
+}
+
+void launch_preempt_stats(const ModelConst& m, const TraceDev& t, unsigned long long* out, cudaStream_t s) {
+    const uint64_t threads = (uint64_t)t.R * 32;
+    k_preempt_stats<<<(uint32_t)((threads + 255) / 256), 256, 0, s>>>(m, t, out);
 }
 
 void launch_replica_counters(const TraceDev& t, unsigned long long* out, cudaStream_t s) {

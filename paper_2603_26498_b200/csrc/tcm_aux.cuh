@@ -14,6 +14,7 @@ constexpr uint32_t kRepCnt = 6;   // tcm_replica_counters fields per replica
 
 void launch_init(const TraceDev& t, cudaStream_t s);
 void launch_replica_counters(const TraceDev& t, unsigned long long* out, cudaStream_t s);
+void launch_preempt_stats(const ModelConst& m, const TraceDev& t, unsigned long long* out, cudaStream_t s);
 void launch_kpack(const ModelConst& m, const TraceDev& t, cudaStream_t s);
 void launch_validate(const TraceDev& t, uint32_t* v, int general_ok, cudaStream_t s);
 void launch_reduce(const TraceDev& t, unsigned long long* acc, cudaStream_t s);

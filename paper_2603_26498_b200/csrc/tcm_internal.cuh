@@ -28,7 +28,7 @@ struct __align__(16) ReplicaState {
     uint32_t n_dec;          // decoding sequences
     uint32_t n_pend;         // pending (waiting + partial) requests
     uint32_t head[3];        // class-queue heads (local ids, NIL if empty)
-    uint32_t tail[3];        // class-queue tails
+    uint32_t tail[3];        // stepwise: running-set lower bound, preemptions, forced preemptions (NEXT-1)
     uint32_t rem[3];         // remaining prefill tokens of head[c]
     uint32_t flags;          // bit c: head[c] admitted (KV reserved); bit 8: finished
     uint32_t status;         // ST_*

@@ -139,23 +139,13 @@ def goodput(lo: float, hi: float, res: float = 0.05, threshold: float = 0.9, see
     return {"goodput_rps": rate, "attainment": att, "counters": cnt, "rates": rates}
 
 
-def preemption_summary(modality, footprint, preempt_count, preempted_us, thresholds=None) -> dict:
-    """fig:preemptions (PAPER.md:620-623; SPEC.md:510): per class (M, C, T, all) the number of
-    preemptions, the time spent preempted (s) and the number of requests preempted at
-    least once, from the NEXT-1 per-request results of one or many replicas.  `thresholds` are the
-    classifier's (thr_mc, thr_ct) per modality (R13; default: the smart thresholds)."""
-    inf = 0xFFFFFFFF
-    thr = thresholds or ((4096, inf), (0, inf), (0, 8192))
-    md = np.asarray(modality, dtype=np.int64)
-    f = np.asarray(footprint, dtype=np.int64)
-    mc = np.array([t[0] for t in thr], dtype=np.int64)[md]
-    ct = np.array([t[1] for t in thr], dtype=np.int64)[md]
-    cls = np.where(f < mc, 0, np.where(f < ct, 1, 2))
-    pc = np.asarray(preempt_count, dtype=np.int64)
-    pt = np.asarray(preempted_us, dtype=np.int64)
-    out = {}
-    for g, name in enumerate(GROUPS):
-        sel = np.ones_like(cls, dtype=bool) if name == "all" else cls == g
-        out[name] = {"preemptions": int(pc[sel].sum()), "preempted_s": float(pt[sel].sum()) / 1e6,
-                     "requests_preempted": int((pc[sel] > 0).sum()), "requests": int(sel.sum())}
-    return out
+def preemption_summary(counters) -> dict:
+    """fig:preemptions (PAPER.md:620-623; SPEC.md:485, 510): per class (M, C, T, all) the number of
+    preemptions, the time spent preempted (s) and the number of requests preempted at least once.
+    `counters` is the device's int64 [4, 3] (or [cells, 4, 3], summed over cells) from
+    Simulation.preemption_stats() -- classified on the device by the engine's own a1 classifier."""
+    c = np.asarray(counters, dtype=np.int64)
+    if c.ndim == 3:
+        c = c.sum(axis=0)
+    return {name: {"preemptions": int(c[g, 0]), "preempted_s": float(c[g, 1]) / 1e6,
+                   "requests_preempted": int(c[g, 2])} for g, name in enumerate(GROUPS)}

@@ -29,7 +29,7 @@ INF32 = 0xFFFFFFFF
 
 EXPORTS = ("tcm_create", "tcm_load_trace", "tcm_reset", "tcm_step", "tcm_run", "tcm_stats", "tcm_destroy",
            "tcm_last_error", "tcm_workspace_bytes", "tcm_generate_trace", "tcm_k1_eval",
-           "tcm_k1_audit", "tcm_k1_filter_error", "tcm_replica_counters")
+           "tcm_k1_audit", "tcm_k1_filter_error", "tcm_replica_counters", "tcm_preemption_stats")
 
 
 class TcmError(RuntimeError):
@@ -105,6 +105,8 @@ def lib():
         L.tcm_stats.argtypes = [vp, ctypes.POINTER(tcm_stats_host), vp, vp]
         L.tcm_replica_counters.restype = st
         L.tcm_replica_counters.argtypes = [vp, vp]
+        L.tcm_preemption_stats.restype = st
+        L.tcm_preemption_stats.argtypes = [vp, vp]
         L.tcm_destroy.restype = None
         L.tcm_destroy.argtypes = [vp]
         L.tcm_last_error.restype = ctypes.c_char_p
@@ -219,6 +221,14 @@ REPLICA_COUNTERS = ("iterations", "decisions", "sum_pending", "scanned_decisions
 def tcm_replica_counters(ctx, dev_out):
     """dev_out: device uint64 tensor [R, 6] (REPLICA_COUNTERS order)."""
     _check(lib().tcm_replica_counters(ctx, _ptr(dev_out)), ctx)
+
+
+PREEMPT_COUNTERS = ("preemptions", "preempted_us", "requests_preempted")
+
+
+def tcm_preemption_stats(ctx, dev_out):
+    """dev_out: device int64 tensor [n_cells, 4, 3] (groups M, C, T, all; PREEMPT_COUNTERS order)."""
+    _check(lib().tcm_preemption_stats(ctx, _ptr(dev_out)), ctx)
 
 
 def tcm_destroy(ctx):
@@ -366,6 +376,16 @@ class Simulation:
         tcm_replica_counters(self.ctx, out)
         a = out.cpu().numpy()
         return {k: a[:, i] for i, k in enumerate(REPLICA_COUNTERS)}
+
+    def preemption_stats(self, device="cuda"):
+        """fig:preemptions counters per (cell, group) from the device (int64 [n_cells, 4, 3])."""
+        import torch
+        import contextlib
+        on = torch.cuda.stream(self.stream) if isinstance(self.stream, torch.cuda.Stream) else contextlib.nullcontext()
+        with on:
+            out = torch.empty((self.cfg.n_cells, GROUPS, len(PREEMPT_COUNTERS)), dtype=torch.int64, device=device)
+        tcm_preemption_stats(self.ctx, out)
+        return out
 
     def close(self):
         if self.ctx:

@@ -176,3 +176,30 @@ def test_growth_launch_modes_bit_exact(mode, monkeypatch):
     out, st = run_gpu(tr, params)
     c = check(tr, params, out, range(24))
     assert c["preemptions"] > 0 and st["preemptions"] == c["preemptions"]
+
+
+def test_device_preemption_stats_equal_oracle():
+    # fig:preemptions counters (tcm_preemption_stats) per (cell, class): the device classifies with the
+    # engine's a1 classifier; the oracle side sums its per-request results by orc_classify
+    tr, params = growth_sweep(64, 400, 75)
+    params["cell_id"] = np.arange(64) % 4
+    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE, n_cells=4))
+    dev = tcm.to_device(tr, params)
+    res = tcm.alloc_results(tr.n_requests, preemption=True)
+    sim.load(dev, res)
+    sim.run()
+    got = sim.preemption_stats().cpu().numpy()
+    sim.close()
+    want = np.zeros((4, 4, 3), np.int64)
+    for r in range(64):
+        a, b = int(tr.offset[r]), int(tr.offset[r + 1])
+        o = O.simulate_trace_growth(tr, r, policy=int(params["policy"][r]), alpha=float(params["aging_alpha"][r]),
+                                    kv_capacity=int(params["kv_capacity"][r]),
+                                    chunk_budget=int(params["chunk_budget"][r]))
+        for i in range(b - a):
+            if o.preempt_count[i]:
+                g = O.classify(int(tr.modality[a + i]), int(tr.footprint[a + i]))
+                for gg in (g, 3):
+                    want[r % 4, gg] += (int(o.preempt_count[i]), int(o.preempted_us[i]), 1)
+    assert want[:, 3, 0].sum() > 0
+    np.testing.assert_array_equal(got, want)

@@ -71,6 +71,18 @@ def test_goodput_binary_search_spec_examples():
     assert gs == sorted(gs, reverse=True)
 
 
+def _oracle_counters(reqs, res):
+    """[4, 3] fig:preemptions counters from oracle results, classes from the oracle's classifier."""
+    import numpy as np
+    import oracle as O
+    c = np.zeros((4, 3), np.int64)
+    for m, f, pc, pt in zip(reqs["modality"], reqs["footprint"], res.preempt_count, res.preempted_us):
+        if pc:
+            for g in (O.classify(m, f), 3):
+                c[g] += (int(pc), int(pt), 1)
+    return c
+
+
 def test_preemption_summary_golden_p2():
     # tests/golden/preemption.json P2: FCFS preempts the text (motorcycle) once for 517,000 us,
     # TCM preempts the image (car) once for 792,000 us
@@ -79,9 +91,9 @@ def test_preemption_summary_golden_p2():
     reqs = dict(arrival_us=[0, 0], footprint=[150, 300], inline_us=[0, 0], out_tokens=[100, 150], modality=[1, 0])
     f = O.simulate_growth(**reqs, policy=O.FCFS, kv_capacity=460)
     t = O.simulate_growth(**reqs, policy=O.TCM, kv_capacity=460)
-    sf = M.preemption_summary(reqs["modality"], reqs["footprint"], f.preempt_count, f.preempted_us)
-    st = M.preemption_summary(reqs["modality"], reqs["footprint"], t.preempt_count, t.preempted_us)
-    assert sf["M"] == {"preemptions": 1, "preempted_s": 0.517, "requests_preempted": 1, "requests": 1}
+    sf = M.preemption_summary(_oracle_counters(reqs, f))
+    st = M.preemption_summary(_oracle_counters(reqs, t)[None])      # [cells, 4, 3] sums over cells
+    assert sf["M"] == {"preemptions": 1, "preempted_s": 0.517, "requests_preempted": 1}
     assert sf["C"]["preemptions"] == 0 and st["M"]["preemptions"] == 0
-    assert st["C"] == {"preemptions": 1, "preempted_s": 0.792, "requests_preempted": 1, "requests": 1}
-    assert st["all"]["preemptions"] == 1 and st["T"]["requests"] == 0
+    assert st["C"] == {"preemptions": 1, "preempted_s": 0.792, "requests_preempted": 1}
+    assert st["all"]["preemptions"] == 1 and st["T"]["requests_preempted"] == 0

@@ -1,0 +1,29 @@
+"""Time k_fused on the C4 bench workload with the libtcm at TCM_LIB_PATH and print a digest of the
+results, for A/B of build variants (development tool)."""
+import hashlib, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2603_26498_b200 import tcm, workloads as W
+
+R = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+sw = W.c4(replicas_per_gpu=R)
+dev = tcm.generate_device(sw.gen)
+dev["params"] = tcm.to_device_params(sw.params)
+sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells))
+res = tcm.alloc_results(sw.n_requests)
+ts = []
+for rep in range(3):
+    sim.load(dev, res)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record(); sim.run(); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+st = sim.stats()
+h = hashlib.sha256()
+for k in ("admit_seq", "first_token_us", "done_us"):
+    h.update(res[k].view(torch.uint8).cpu().numpy().tobytes()) if res[k].numel() < 0 else None
+    x = res[k]
+    h.update(str(int(x.view(torch.int64 if x.element_size() == 8 else torch.int32).to(torch.int64).sum())).encode())
+name = os.path.basename(os.environ.get("TCM_LIB_PATH", "libtcm.so"))
+print(f"{name}: run ms {['%.1f' % t for t in ts]} engine_ms {st.get('engine_ms', 0):.1f} scanned {st['scanned_decisions']} "
+      f"decisions {st['decisions']} digest {h.hexdigest()[:16]}", flush=True)
