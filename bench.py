@@ -134,8 +134,16 @@ def dist_init(args):
         import torch.distributed as dist
         if args.impl == "tcm":
             import torch
-            torch.cuda.set_device(local)
-            dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
+            ngpu = torch.cuda.device_count()
+            if world <= ngpu:                # one process per GPU, NCCL over NVLink
+                torch.cuda.set_device(local)
+                dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
+                args.collective = "nccl"
+            else:                            # more ranks than GPUs (a functional run on a smaller box):
+                local = local % ngpu         # ranks share GPUs; NCCL refuses two ranks on one device,
+                torch.cuda.set_device(local) # so the int64 all-reduce goes through gloo (CUDA tensors)
+                dist.init_process_group(backend="gloo")
+                args.collective = f"gloo ({world} ranks sharing {ngpu} GPU(s): functional, not a scaling point)"
         else:
             dist.init_process_group(backend="gloo")
         assert dist.get_world_size() == args.gpus
@@ -418,7 +426,7 @@ def run_tcm(args, rank, world, local):
         "scanned_decisions_per_s": scan_s,
         "config": {"workload": wl, "n_cells": sw.n_cells,
                    "replicas_per_gpu": args.replicas, "requests_per_replica": args.requests,
-                   "requests_per_step": int(tot[0] / args.steps), "parallelism": f"replicas sharded x{world}",
+                   "requests_per_step": int(tot[0] / args.steps), "parallelism": f"replicas sharded x{world}", "collective": getattr(args, "collective", "none (1 rank)"),
                    "l2": "inputs larger than L2 (trace %.1f GB per GPU)" % (N * 19 / 1e9)},
         "roofline": {"kernel": "k_fused", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -637,14 +645,14 @@ def bench_next1(args, dev, stream):
     pst = sim.preemption_stats(device=dev).cpu().numpy()          # [cells][M, C, T, all][3]
     cell_pol = np.array([c["policy"] for c in sw.cells])
     by = {}
-    for name, p in (("FCFS", tcm.POLICY_FCFS), ("TCM", tcm.POLICY_TCM)):
+    for name, p in (("FCFS", tcm.POLICY_FCFS), ("EDF", tcm.POLICY_EDF), ("TCM", tcm.POLICY_TCM)):
         summ = M.preemption_summary(pst[cell_pol == p])
         by[name] = {"preemptions": summ["all"]["preemptions"], "motorcycle_preemptions": summ["M"]["preemptions"],
                     "requests_preempted": summ["all"]["requests_preempted"],
                     "preempted_s": {g: round(summ[g]["preempted_s"], 3) for g in ("M", "C", "T")}}
     sim.close()
     return {"workload": f"C4-growth: {sw.n_replicas} replicas x {args.next1_requests} requests (C4 cells, "
-                        "KV growth + preemption), stepwise engine",
+                        "KV growth + preemption; FCFS, EDF with R34 inversion preemption, TCM), stepwise engine",
             "value": sw.n_requests / (ms / 1e3), "unit": "requests/s", "ms": ms,
             "decisions_per_s": st["decisions"] / (ms / 1e3), "iterations": st["iterations"],
             "preemptions": st["preemptions"], "forced_preemptions": st["forced_preemptions"],
@@ -769,7 +777,7 @@ def main():
     ap.add_argument("--step-reps", type=int, default=3)
     ap.add_argument("--skip-step", action="store_true")
     ap.add_argument("--skip-next1", action="store_true")
-    ap.add_argument("--next1-replicas", type=int, default=1024)
+    ap.add_argument("--next1-replicas", type=int, default=1536)
     ap.add_argument("--next1-requests", type=int, default=1000)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")

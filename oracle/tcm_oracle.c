@@ -409,6 +409,13 @@ int orc_simulate(const orc_model* m, const orc_replica* r, uint32_t n,
 /* ------------------------------------------------------------------------------ */
 enum { PH_WAIT = 1, PH_PREFILL = 2, PH_DECODE = 3, PH_DONE = 4 };
 
+/* EDF key of request i: its deadline x den = arrival*den + num*iso_e2e (R27). */
+static uint64_t orc_edf_key(const orc_model* m, const orc_replica* r, uint32_t i, const uint64_t* arrival,
+                            const uint32_t* f, const uint32_t* inl, const uint16_t* out)
+{
+    return arrival[i] * m->slo_den + m->slo_num * orc_iso_e2e(m, r->chunk_budget, f[i], inl[i], out[i]);
+}
+
 int orc_simulate_growth(const orc_model* m, const orc_replica* r, uint32_t n,
                         const uint64_t* arrival, const uint32_t* f, const uint32_t* inl,
                         const uint16_t* out, const uint8_t* mod, uint32_t* admit_seq,
@@ -437,9 +444,11 @@ int orc_simulate_growth(const orc_model* m, const orc_replica* r, uint32_t n,
     uint32_t* held = (uint32_t*)calloc(n + 1, 4);
     uint32_t* gen = (uint32_t*)calloc(n + 1, 4);
     uint64_t* pstart = (uint64_t*)calloc(n + 1, 8);
+    uint64_t* pre_it = (uint64_t*)calloc(n + 1, 8);    /* EDF inversion victims: iteration + 1 (R34) */
     orc_entry* order = (orc_entry*)malloc(sizeof(orc_entry) * (n + 1));
-    if (!ph || !admitted || !emitted || !rem || !held || !gen || !pstart || !order) {
-        free(ph); free(admitted); free(emitted); free(rem); free(held); free(gen); free(pstart); free(order);
+    if (!ph || !admitted || !emitted || !rem || !held || !gen || !pstart || !pre_it || !order) {
+        free(ph); free(admitted); free(emitted); free(rem); free(held); free(gen); free(pstart); free(pre_it);
+        free(order);
         return -1;
     }
     for (uint32_t i = 0; i < n; ++i) { pcount[i] = 0; ptime[i] = 0; }
@@ -543,6 +552,49 @@ int orc_simulate_growth(const orc_model* m, const orc_replica* r, uint32_t n,
             if (left == 0) break;
             if (ph[i] == PH_WAIT) {
                 if (blocked) continue;
+                if (pre_it[i] == iter + 1) continue;      /* preempted for an earlier deadline just now (R34) */
+                if ((uint64_t)rem[i] > kv_free && r->policy == ORC_EDF) {
+                    /* R34 EDF priority inversion: running requests that come
+                     * after i in EDF order (deadline, arrival, id) are preempted, latest first, until i
+                     * fits -- only if preempting all of them would make it fit. */
+                    const uint64_t dw = order[q].dl;
+                    uint64_t avail = kv_free;
+                    for (uint32_t v = 0; v < nxt; ++v) {
+                        if (ph[v] != PH_PREFILL && ph[v] != PH_DECODE) continue;
+                        const uint64_t dv = orc_edf_key(m, r, v, arrival, f, inl, out);
+                        if (dv > dw || (dv == dw && (arrival[v] > arrival[i] || (arrival[v] == arrival[i] && v > i))))
+                            avail += held[v];
+                    }
+                    while (avail >= rem[i] && (uint64_t)rem[i] > kv_free) {
+                        uint32_t v = UINT32_MAX;
+                        uint64_t vd = 0;
+                        for (uint32_t u = 0; u < nxt; ++u) {
+                            if (ph[u] != PH_PREFILL && ph[u] != PH_DECODE) continue;
+                            const uint64_t du = orc_edf_key(m, r, u, arrival, f, inl, out);
+                            const int after = du > dw || (du == dw && (arrival[u] > arrival[i] ||
+                                                                       (arrival[u] == arrival[i] && u > i)));
+                            /* the latest in EDF order among them: max (deadline, arrival, id) */
+                            if (after && (v == UINT32_MAX || du > vd ||
+                                          (du == vd && (arrival[u] > arrival[v] || (arrival[u] == arrival[v] && u > v))))) {
+                                v = u;
+                                vd = du;
+                            }
+                        }
+                        if (ph[v] == PH_DECODE) {
+                            n_dec--;                      /* it does not decode in this iteration */
+                            rem[v] = held[v] - 1;         /* recompute what it held before this iteration */
+                        } else {
+                            rem[v] = held[v];
+                        }
+                        kv_free += held[v];               /* including this iteration's decode token */
+                        held[v] = 0;
+                        ph[v] = PH_WAIT;
+                        pre_it[v] = iter + 1;
+                        pcount[v]++;
+                        pstart[v] = clock;
+                        (*n_preempt)++;
+                    }
+                }
                 if ((uint64_t)rem[i] > kv_free) { blocked = !r->admit_skip; continue; }
                 ph[i] = PH_PREFILL;
                 held[i] = rem[i];
@@ -603,7 +655,8 @@ int orc_simulate_growth(const orc_model* m, const orc_replica* r, uint32_t n,
     }
     cnt->admitted = seq;
     cnt->final_clock = clock;
-    free(ph); free(admitted); free(emitted); free(rem); free(held); free(gen); free(pstart); free(order);
+    free(ph); free(admitted); free(emitted); free(rem); free(held); free(gen); free(pstart); free(pre_it);
+    free(order);
     return status;
 }
 

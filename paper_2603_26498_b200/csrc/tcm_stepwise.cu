@@ -243,6 +243,7 @@ struct GroupSmem {
     uint64_t left, tok, inl;
     uint32_t thi;
     int npart, ndone, mode, pass_more, blocked, has_th;
+    int inv_any, inv_dec;   // NEXT-3 EDF inversion (R34): preempted this iteration; decoding victims among them
 };
 
 template <int G>
@@ -461,6 +462,115 @@ __device__ __noinline__ void sw_preempt(const ModelConst& m, const TraceDev& t, 
     __syncwarp();
 }
 
+// NEXT-3 EDF priority inversion under TCM_KV_GROWTH (reading R34):
+// over the current batch of candidates (lane = rank in EDF order, li = id), the first waiting
+// request m that does not fit (and is reached by the budget, admissions not yet blocked) preempts
+// running requests that come after it in EDF order (deadline x den, id), latest first, until the
+// admissions up to m fit -- if preempting all of them would.  Repeats for the next misfit.  A
+// victim frees what it holds (a decoding one including this iteration's token: it does not decode
+// now), is recomputed later (R30) and is excluded for the rest of this iteration (RS_FT on a request
+// without RS_RES; a5 clears it).  Warp-collective on the group's first warp; returns the new kv_free.
+__device__ __noinline__ uint64_t sw_edf_invert(const TraceDev& t, uint32_t r, uint64_t base, uint8_t* rs,
+                                               uint32_t* rem, uint32_t li, bool valid, bool blocked_prev,
+                                               uint64_t left, uint64_t kv, uint32_t hi, ReplicaState& st,
+                                               int& inv_any, int& inv_dec, int lane) {
+    const uint64_t* dl = t.deadline + base;
+    const uint32_t* fp = t.footprint + base;
+    for (;;) {
+        const uint8_t sb = valid ? rs[li] : 0;
+        const bool v = valid && !((sb & RS_FT) && !(sb & RS_RES));
+        const bool res = v && (sb & RS_RES);
+        const bool prev = v && (sb & RS_PREV);
+        const uint32_t rr = v ? ((res || prev) ? rem[li] : fp[li]) : 0;
+        const uint32_t f = prev ? rr : (v ? fp[li] : 0);
+        const bool waiting = v && !res;
+        const uint64_t cumf = warp_incl_scan64(waiting ? f : 0, lane);
+        const bool kv_ok = waiting && !blocked_prev && cumf <= kv;
+        const bool part = v && (res || kv_ok);
+        const uint64_t incl = warp_incl_scan64(part ? rr : 0, lane);
+        const bool misfit = waiting && !blocked_prev && !kv_ok && incl - (part ? rr : 0) < left;
+        const uint32_t mm = __ballot_sync(0xFFFFFFFFu, misfit);
+        if (!mm) return kv;
+        const int ml = __ffs(mm) - 1;
+        const uint64_t need = __shfl_sync(0xFFFFFFFFu, cumf, ml) - kv;
+        const uint32_t im = __shfl_sync(0xFFFFFFFFu, li, ml);
+        const uint64_t dm = dl[im];
+        // running requests after (dm, im): decoding (holding incl. this iteration's token) or partial
+        auto holding = [&](uint32_t i, uint8_t s) -> uint64_t {
+            return (s & RS_DEC) ? (uint64_t)t.kvfin[base + i] - (t.fin[base + i] - st.iter) + 1 : t.kvres[base + i];
+        };
+        uint64_t avail = 0;
+        for (uint32_t c0 = 0; c0 < hi; c0 += 32) {
+            const uint32_t i = c0 + lane;
+            const uint8_t s = i < hi ? rs[i] : 0;
+            if ((s & (RS_RES | RS_DEC)) && (dl[i] > dm || (dl[i] == dm && i > im))) avail += holding(i, s);
+        }
+        avail = warp_sum64(avail);
+        if (avail < need) return kv;                           // m blocks (R6)
+        uint64_t got = 0;
+        while (got < need) {
+            uint64_t bd = 0;
+            uint32_t bi = NIL;
+            for (uint32_t c0 = 0; c0 < hi; c0 += 32) {         // the latest in EDF order
+                const uint32_t i = c0 + lane;
+                const uint8_t s = i < hi ? rs[i] : 0;
+                if ((s & (RS_RES | RS_DEC)) && (dl[i] > dm || (dl[i] == dm && i > im)) &&
+                    (bi == NIL || dl[i] > bd || (dl[i] == bd && i > bi))) {
+                    bd = dl[i];
+                    bi = i;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t od = __shfl_xor_sync(0xFFFFFFFFu, bd, o);
+                const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+                if (oi != NIL && (bi == NIL || od > bd || (od == bd && oi > bi))) {
+                    bd = od;
+                    bi = oi;
+                }
+            }
+            uint64_t freed = 0;
+            if (lane == 0) {
+                const uint32_t vv = bi;
+                const uint8_t s = rs[vv];
+                freed = holding(vv, s);
+                if (s & RS_DEC) {
+                    const uint64_t F = t.fin[base + vv];
+                    const uint32_t togo = (uint32_t)(F - st.iter);
+                    rem[vv] = t.kvfin[base + vv] - togo;         // what it held before this iteration
+                    t.genp[base + vv] = (uint32_t)t.out[base + vv] - togo;
+                    const uint32_t slot = (uint32_t)(F & (kCalSlots - 1));
+                    uint32_t* cal = t.cal + (size_t)r * kCalSlots;
+                    uint32_t* link = t.link + base;
+                    uint32_t prv = NIL, cur = cal[slot];
+                    while (cur != vv) {
+                        prv = cur;
+                        cur = link[cur];
+                    }
+                    if (prv == NIL) cal[slot] = link[vv];
+                    else link[prv] = link[vv];
+                    if (cal[slot] == NIL) t.occ[(size_t)r * kCalWords + (slot >> 5)] &= ~(1u << (slot & 31));
+                    st.n_dec--;
+                    st.n_pend++;
+                    inv_dec++;
+                    rs[vv] = (uint8_t)((s & ~RS_DEC) | RS_PEND | RS_FT);
+                } else {
+                    rem[vv] = t.kvres[base + vv];
+                    rs[vv] = (uint8_t)((s & ~RS_RES) | RS_FT);
+                }
+                t.pcount[base + vv]++;
+                t.pstart[base + vv] = st.clock;
+                st.tail[1]++;
+                if (vv < st.head[0]) st.head[0] = vv;
+                inv_any = 1;
+            }
+            __syncwarp();
+            got += __shfl_sync(0xFFFFFFFFu, freed, 0);
+        }
+        kv += got;
+    }
+}
+
 }  // namespace
 
 // GR: some replica of the trace runs TCM_KV_GROWTH (NEXT-1); the plain instantiation compiles
@@ -550,6 +660,8 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 gsm.has_th = 0;
                 gsm.npart = 0;
                 gsm.ndone = 0;
+                gsm.inv_any = 0;
+                gsm.inv_dec = 0;
             }
         }
         gsync<G, CL>();
@@ -875,11 +987,24 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
 #pragma unroll 1
                     for (int w = 1; w < G; ++w) warp_merge(lk, li, sm.wkey[w][lane], sm.wid[w][lane], lane);
                 }
-                const bool valid = li != NIL;
+                bool valid = li != NIL;
                 const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
                 const uint64_t left = gsm.left;
-                const uint64_t kv = gsm.st.kv_free;
                 const bool blocked_prev = gsm.blocked;
+                if (GR && growth && edf && !skip) {           // NEXT-3 EDF priority inversion (R34)
+                    int ia = 0, idc = 0;
+                    const uint64_t kvn = sw_edf_invert(t, r, base, rs, rem, li, valid, blocked_prev, left,
+                                                       gsm.st.kv_free, hi, gsm.st, ia, idc, lane);
+                    __syncwarp();
+                    if (lane == 0) {
+                        gsm.st.kv_free = kvn;
+                        gsm.inv_any |= ia;
+                        gsm.inv_dec += idc;
+                    }
+                    __syncwarp();
+                    if (valid && (rsc[li] & (RS_FT | RS_RES)) == RS_FT) valid = false;   // a victim of this iteration
+                }
+                const uint64_t kv = gsm.st.kv_free;
                 uint32_t f = 0, rr = 0, il = 0;
                 bool res = false, prev = false;
                 if (valid) {
@@ -1011,8 +1136,9 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 st.head[1]--;
                 st.decisions++;
                 st.scanned++;
-                st.sum_pending += st.n_pend;
-                st.max_pending = st.n_pend > st.max_pending ? st.n_pend : st.max_pending;
+                const uint32_t np = st.n_pend - (uint32_t)gsm.inv_dec;   // the pending set when ordered (R17)
+                st.sum_pending += np;
+                st.max_pending = np > st.max_pending ? np : st.max_pending;
                 const Cal cal{t.cal + (size_t)r * kCalSlots, t.occ + (size_t)r * kCalWords};
                 cal_process(cal, t.link + base, st.iter, st.clock, growth ? t.kvfin + base : fp, t.done + base, st,
                             growth ? rs : nullptr);
@@ -1068,9 +1194,14 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 for (int q = lane; q < nd; q += 32) stamp(gsm.done[q]);
             } else {
                 for (uint32_t i = lo + lane; i < hi; i += 32)
-                    if (rs[i] & RS_FT) stamp(i);
+                    if ((rs[i] & (RS_FT | RS_RES)) == (RS_FT | RS_RES)) stamp(i);
             }
             __syncwarp();
+            if (GR && gsm.inv_any) {                      // R34 victims may be admitted again from the next iteration
+                for (uint32_t i = st.head[0] + lane; i < hi; i += 32)
+                    if ((rs[i] & (RS_FT | RS_RES)) == RS_FT) rs[i] = (uint8_t)(rs[i] & ~RS_FT);
+                __syncwarp();
+            }
             kv_add = warp_sum64(kv_add);
             n_dec_add = warp_sum64(n_dec_add);
             done_add = warp_sum64(done_add);

@@ -42,6 +42,7 @@ def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
          for i, (a, f, il, o, m) in enumerate(reqs)]
     clock, free, seq = 0, kv, 0
     near_tie = False
+    it_no = 0                                             # engine iterations (R34 marks victims)
     while True:
         for r in R:                                       # step 1: ingest
             if r["state"] == "future" and r["arr"] <= clock:
@@ -95,13 +96,29 @@ def run(reqs, policy, alpha=1.0, kv=131072, B=2048, c0=5000, cp=20, cd=500,
         else:
             order = sorted(pend, key=lambda r: (r["arr"], r["id"]))
         left, blocked, tok, inl = budget, False, 0, 0     # step 6 (R6, R7)
+        it_no += 1
         for r in order:
             if left == 0:
                 break
             if r["state"] == "waiting":
                 need = r["rem"] if growth else r["f"]
-                if blocked:
+                if blocked or r.get("pre_it") == it_no:
                     continue
+                if need > free and growth and policy == 2:
+                    # R34: EDF preempts running requests with a later deadline (deadline, arrival, id),
+                    # latest first, until the earlier-deadline request fits -- if they can make it fit
+                    ek = lambda x: (dl(x), x["arr"], x["id"])
+                    later = sorted((x for x in R if x["state"] in ("partial", "decoding") and ek(x) > ek(r)),
+                                   key=ek, reverse=True)
+                    if free + sum(x["held"] for x in later) >= need:
+                        for v in later:
+                            if need <= free:
+                                break
+                            free += v["held"]
+                            v["rem"] = v["held"] - 1 if v["state"] == "decoding" else v["held"]
+                            v["held"], v["state"], v["since"], v["pre_it"] = 0, "waiting", clock, it_no
+                            v["npre"] += 1
+                        dec = [x for x in dec if x["state"] == "decoding"]
                 if need > free:
                     blocked = not skip
                     continue

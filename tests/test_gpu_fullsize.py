@@ -242,8 +242,9 @@ def _oracle_growth_job(job):
 
 
 def test_c4_growth_bench_config_sampled_bit_exact():
-    # NEXT-1 at the size bench.py times (C4-growth, 1,024 x 1,000, stepwise engine): one replica per cell
-    sw = W.c4_growth(0, 1, replicas_per_gpu=1024, n_requests=1000)
+    # NEXT-1 at the size bench.py times (C4-growth, 1,536 x 1,000, stepwise engine; FCFS, TCM and EDF
+    # cells): one replica per cell
+    sw = W.c4_growth(0, 1, replicas_per_gpu=1536, n_requests=1000)
     dev = tcm.generate_device(sw.gen)
     dev["params"] = torch.from_numpy(sw.params.view(np.uint8)).cuda()
     res = tcm.alloc_results(sw.n_requests, preemption=True)

@@ -43,7 +43,8 @@ def run_gpu(tr, params, engine=tcm.ENGINE_STEPWISE, step=None):
     return out, st
 
 
-def growth_sweep(R, n, seed, kvs=(16384, 32768), rates=(1.0, 3.0, 6.0), mixes=((0.5, 0.2, 0.3), (0.7, 0.25, 0.05))):
+def growth_sweep(R, n, seed, kvs=(16384, 32768), rates=(1.0, 3.0, 6.0), mixes=((0.5, 0.2, 0.3), (0.7, 0.25, 0.05)),
+                 policies=(tcm.POLICY_FCFS, tcm.POLICY_TCM)):
     rng = np.random.default_rng(seed)
     reps, params = [], tcm.make_params(R)
     for r in range(R):
@@ -52,7 +53,7 @@ def growth_sweep(R, n, seed, kvs=(16384, 32768), rates=(1.0, 3.0, 6.0), mixes=((
         nr = int(rng.integers(max(1, n // 3), n + 1))
         reps.append(T.make_replica(seed, r, nr, float(rng.choice(rates)), mix, kv - 2048))   # f + out - 1 <= kv
         params[r]["kv_capacity"] = kv
-        params[r]["policy"] = rng.choice([tcm.POLICY_FCFS, tcm.POLICY_TCM])
+        params[r]["policy"] = rng.choice(list(policies))
         params[r]["aging_alpha"] = rng.choice([0.0, 2.0**-7, 1.0, 16.0])
         params[r]["chunk_budget"] = rng.choice([256, 2048, 8192])
         params[r]["flags"] = tcm.KV_GROWTH
@@ -88,7 +89,8 @@ def check(tr, params, out, replicas):
 def test_hand_worked_preemption_gpu(case):
     tr = T.from_requests(case["requests"])
     params = tcm.make_params(1, kv_capacity=case["kv"])
-    params["policy"] = tcm.POLICY_FCFS if case["policy"] == "FCFS" else tcm.POLICY_TCM
+    params["policy"] = {"FCFS": tcm.POLICY_FCFS, "TCM": tcm.POLICY_TCM, "EDF": tcm.POLICY_EDF}[case["policy"]]
+    params["chunk_budget"] = case.get("B", 2048)
     params["flags"] = tcm.KV_GROWTH
     out, st = run_gpu(tr, params)
     e = case["expect"]
@@ -203,3 +205,16 @@ def test_device_preemption_stats_equal_oracle():
                     want[r % 4, gg] += (int(o.preempt_count[i]), int(o.preempted_us[i]), 1)
     assert want[:, 3, 0].sum() > 0
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("launch", [None, "1", "8"])
+def test_edf_inversion_preemption_bit_exact(launch, monkeypatch):
+    # NEXT-3 EDF with its priority-inversion preemption (R34) under KV growth, every
+    # launch mode of the stepwise engine, against the oracle
+    if launch:
+        monkeypatch.setenv("TCM_SW_GROUP", launch)
+    tr, params = growth_sweep(48, 400, 76, policies=(tcm.POLICY_EDF,))
+    out, st = run_gpu(tr, params)
+    c = check(tr, params, out, range(48))
+    assert c["preemptions"] > 0 and st["preemptions"] == c["preemptions"]
+    assert st["decisions"] == c["decisions"] and st["sum_pending"] == c["sum_pending"]

@@ -24,7 +24,8 @@ def run(reqs, policy, **kw):
 
 @pytest.mark.parametrize("case", GOLD["cases"], ids=[c["name"] for c in GOLD["cases"]])
 def test_hand_worked_preemption(case):
-    tr, r = run(case["requests"], O.FCFS if case["policy"] == "FCFS" else O.TCM, kv_capacity=case["kv"])
+    pol = {"FCFS": O.FCFS, "TCM": O.TCM, "EDF": O.EDF}[case["policy"]]
+    tr, r = run(case["requests"], pol, kv_capacity=case["kv"], chunk_budget=case.get("B", 2048))
     e = case["expect"]
     assert r.status == 0
     assert r.first_token_us.tolist() == e["first"]
@@ -95,7 +96,7 @@ def test_tcm_spares_motorcycles_vs_fcfs():
 
 def test_brute_force_vs_declarative_engine():
     rng = random.Random(2027)
-    checked = 0
+    checked = edf_pre = 0
     for case in range(400):
         n = rng.randint(1, 6)
         kv = rng.choice([40, 64, 100])
@@ -105,7 +106,7 @@ def test_brute_force_vs_declarative_engine():
             f = rng.randint(1, 30)
             out = rng.randint(1, kv - f + 1)
             reqs.append([t, f, rng.choice([0, 0, 700]), out, rng.randint(0, 2)])
-        pol = rng.choice([O.FCFS, O.TCM])
+        pol = rng.choice([O.FCFS, O.TCM, O.EDF])          # EDF: R34 priority-inversion preemption
         B = rng.choice([1, 3, 8, 64])
         alpha = rng.choice([0.0, 1.0, 64.0])
         sp = spec_engine.run([tuple(x) for x in reqs], pol, alpha=alpha, kv=kv, B=B, growth=True)
@@ -119,4 +120,6 @@ def test_brute_force_vs_declarative_engine():
         assert r.preempt_count.tolist() == sp["preempt_count"], (case, reqs)
         assert r.preempted_us.tolist() == sp["preempted_us"], (case, reqs)
         checked += 1
+        edf_pre += pol == O.EDF and r.counters["preemptions"] > 0
     assert checked > 350
+    assert edf_pre > 10
