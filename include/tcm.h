@@ -58,8 +58,9 @@ enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1, TCM_POLICY_EDF = 2, TCM_POLICY_N
  * TCM : three class queues + aging priority.  Static priority
  *        is TCM with aging_alpha = 0 (R14).
  * EDF : earliest deadline first, deadline = arrival + (slo_num/slo_den) x isolated E2E
- *       (SPEC.md:399); ordering only, no preemption (NEXT-1).  STEPWISE only:
- *       its keys are not class-monotone (Lemma L1 does not hold).
+ *       (SPEC.md:399).  With TCM_KV_GROWTH it also preempts running requests
+ *       with a later deadline when an earlier-deadline waiting request does not fit (R34,
+ *       PAPER.md:622).  STEPWISE only: its keys are not class-monotone (Lemma L1 does not hold).
  * NAIVE_AGING: descending waiting time ignoring class, i.e. arrival order. */
 
 /* tcm_replica_params.flags */
