@@ -36,6 +36,13 @@ struct tcm_ctx {
     cudaEvent_t ev[7] = {};              // reset begin/end, engine begin/end, stamp end, k_step begin/end
     bool reset_pending = false;          // ev[0..1] recorded, not yet read
     double reset_ms = 0, engine_ms = 0, stamp_ms = 0;
+    // tcm_step(n <= kGraphMaxIters): the call's launches (budget / k_step or k_fused + stamp, the
+    // events and the active-count copy) replayed as one CUDA graph per n, captured on the second
+    // call with that n (the first one runs eagerly: it also initialises per-device launch caches)
+    struct Graph { uint32_t iters; cudaGraphExec_t exec; uint64_t launches; bool deferred; };
+    std::vector<Graph> graphs;
+    std::vector<uint32_t> graph_seen;
+    uint32_t* h_active = nullptr;        // pinned: the graphs' copy target
 };
 
 namespace {
@@ -74,6 +81,9 @@ void free_allocs(tcm_ctx* c, bool keep = false) {
     }
     c->loaded = false;
     c->sw = StepwiseWorkspace{};
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);   // they captured the old trace's pointers
+    c->graphs.clear();
+    c->graph_seen.clear();
 }
 
 tcm_status dalloc(tcm_ctx* c, void** p, size_t bytes) {
@@ -214,28 +224,89 @@ tcm_status reset_state(tcm_ctx* c) {
     return TCM_OK;
 }
 
-tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
-    bool deferred = false;      // stepwise: k_step events still to be read after the sync below
+constexpr uint32_t kGraphMaxIters = 64;
+
+// Everything one engine call enqueues, ending with the active-count copy to `active_dst`.
+tcm_status enqueue_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active_dst, uint64_t* launches, bool* deferred) {
+    *deferred = false;
     if (c->cfg.engine == TCM_ENGINE_FUSED) TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
     TCM_CUDA(c, cudaEventRecord(c->ev[2], c->s));
     if (c->cfg.engine == TCM_ENGINE_FUSED) {
         launch_fused(c->m, c->t, max_iters, c->d_active, c->s);
         TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
         launch_fused_stamp(c->t, c->s);
-        c->launches += 2;
+        *launches += 2;
     } else {
-        uint64_t l = 0;
         double kms = 0;
-        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, &l, c->ev[5], c->ev[6], &kms,
-                                     &deferred);
+        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, launches, c->ev[5], c->ev[6],
+                                     &kms, deferred);
         c->engine_ms += kms;
-        c->launches += l;
         if (st != TCM_OK) return fail(c, st, "stepwise engine failed: %s", cudaGetErrorString(cudaGetLastError()));
     }
     TCM_CUDA(c, cudaGetLastError());
     if (c->cfg.engine != TCM_ENGINE_FUSED) TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
     TCM_CUDA(c, cudaEventRecord(c->ev[4], c->s));
-    TCM_CUDA(c, cudaMemcpyAsync(active, c->d_active, 4, cudaMemcpyDeviceToHost, c->s));
+    TCM_CUDA(c, cudaMemcpyAsync(active_dst, c->d_active, 4, cudaMemcpyDeviceToHost, c->s));
+    return TCM_OK;
+}
+
+// The graph of a short call (max_iters <= kGraphMaxIters, one k_step chunk), or nullptr.
+const tcm_ctx::Graph* step_graph(tcm_ctx* c, uint32_t max_iters) {
+    if (max_iters > kGraphMaxIters || !c->h_active) return nullptr;
+    for (auto& g : c->graphs)
+        if (g.iters == max_iters) return &g;
+    bool seen = false;
+    for (uint32_t k : c->graph_seen) seen |= k == max_iters;
+    if (!seen) {                                   // first call with this n: eager
+        c->graph_seen.push_back(max_iters);
+        return nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    uint64_t l = 0;
+    bool deferred = false;
+    if (cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return nullptr;
+    tcm_status st = enqueue_engine(c, max_iters, c->h_active, &l, &deferred);
+    cudaError_t e = cudaStreamEndCapture(c->s, &graph);
+    if (st != TCM_OK || e != cudaSuccess || !graph || !deferred) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return nullptr;
+    }
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    c->graphs.push_back({max_iters, exec, l, deferred});
+    return &c->graphs.back();
+}
+
+tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
+    if (const tcm_ctx::Graph* g = step_graph(c, max_iters)) {
+        TCM_CUDA(c, cudaGraphLaunch(g->exec, c->s));
+        TCM_CUDA(c, cudaStreamSynchronize(c->s));
+        *active = *c->h_active;
+        c->launches += g->launches;
+        float ms = 0;
+        if (c->reset_pending) {
+            TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+            c->reset_ms += ms;
+            c->reset_pending = false;
+        }
+        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->cfg.engine == TCM_ENGINE_FUSED ? c->ev[2] : c->ev[5],
+                                         c->cfg.engine == TCM_ENGINE_FUSED ? c->ev[3] : c->ev[6]));
+        c->engine_ms += ms;
+        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
+        c->stamp_ms += ms;
+        return TCM_OK;
+    }
+    bool deferred = false;      // stepwise: k_step events still to be read after the sync below
+    uint64_t l = 0;
+    tcm_status st = enqueue_engine(c, max_iters, active, &l, &deferred);
+    c->launches += l;
+    if (st != TCM_OK) return st;
     TCM_CUDA(c, cudaStreamSynchronize(c->s));
     float ms = 0;
     if (c->reset_pending) {
@@ -271,6 +342,10 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
     if (e == cudaSuccess) e = cudaMalloc(&c->d_acc, kAccN * 8);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 12);
     for (int i = 0; i < 7 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e == cudaSuccess && cudaMallocHost(&c->h_active, 4) != cudaSuccess) {
+        c->h_active = nullptr;                      // no pinned word: short calls run eagerly
+        cudaGetLastError();
+    }
     if (e != cudaSuccess) {
         fail(nullptr, TCM_E_CUDA, "tcm_create: %s", cudaGetErrorString(e));
         cudaFree(c->d_active);
@@ -555,6 +630,7 @@ void tcm_destroy(tcm_ctx* c) {
     cudaFree(c->d_active);
     cudaFree(c->d_acc);
     cudaFree(c->d_val);
+    if (c->h_active) cudaFreeHost(c->h_active);
     delete c;
 }
 

@@ -232,7 +232,10 @@ struct GroupSmem {
     uint32_t part[kMaxPart];
     uint32_t done[kMaxDone];
     // per-warp refine queue: elements whose FP32 bound cannot rule them out of the top-32
-    static constexpr int kQ = 160;
+#ifndef TCM_SW_KQ
+#define TCM_SW_KQ 160
+#endif
+    static constexpr int kQ = TCM_SW_KQ;
     uint32_t qid[G][kQ];
     uint64_t qw[G][kQ];
     uint8_t qc[G][kQ];

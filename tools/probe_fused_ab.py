@@ -6,7 +6,22 @@ import numpy as np, torch
 from paper_2603_26498_b200 import tcm, workloads as W
 
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+order = sys.argv[2] if len(sys.argv) > 2 else "cell"
 sw = W.c4(replicas_per_gpu=R)
+cells = sw.params["cell_id"].astype(np.int64)
+if order != "cell":                 # permutations of the replica -> lane assignment (results are invariant)
+    nc = sw.n_cells
+    per = R // nc
+    idx = np.arange(R).reshape(nc, per)                      # cell-major
+    if order == "mix2":             # a warp = 16 FCFS replicas + 16 TCM replicas of the same (lambda, KV)
+        f, t = idx[:16], idx[16:]
+        perm = np.stack([f.reshape(16, per // 16, 16), t.reshape(16, per // 16, 16)], axis=2).reshape(-1)
+    elif order == "mixall":         # a warp = one replica of every cell (round 1's cyclic layout)
+        perm = idx.T.reshape(-1)
+    elif order == "rev":            # TCM cells first
+        perm = np.concatenate([idx[16:].reshape(-1), idx[:16].reshape(-1)])
+    sw.gen = sw.gen[perm]
+    sw.params = sw.params[perm]
 dev = tcm.generate_device(sw.gen)
 dev["params"] = tcm.to_device_params(sw.params)
 sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells))
@@ -25,5 +40,5 @@ for k in ("admit_seq", "first_token_us", "done_us"):
     x = res[k]
     h.update(str(int(x.view(torch.int64 if x.element_size() == 8 else torch.int32).to(torch.int64).sum())).encode())
 name = os.path.basename(os.environ.get("TCM_LIB_PATH", "libtcm.so"))
-print(f"{name}: run ms {['%.1f' % t for t in ts]} engine_ms {st.get('engine_ms', 0):.1f} scanned {st['scanned_decisions']} "
+print(f"{name} [{order}]: run ms {['%.1f' % t for t in ts]} engine_ms {st.get('engine_ms', 0):.1f} scanned {st['scanned_decisions']} "
       f"decisions {st['decisions']} digest {h.hexdigest()[:16]}", flush=True)
