@@ -59,6 +59,23 @@ __global__ void k_kpack(ModelConst m, TraceDev t) {
         kp.fC2[c] = (float)c2;
         if (k.zero) kp.zero_mask |= 1u << c;
         else if (!(k.p <= 16.0 && fabs(c2) <= 1000.0)) kp.filter_ok = 0;
+        // saturation point: the least w in [1, 2^33] with K1(w) == K1 at the cap (bisection; monotone)
+        const double smax = kp.Smax[c] < kEps ? kEps : kp.Smax[c];
+        const uint64_t sk = (uint64_t)__double_as_longlong(smax);
+        kp.satkey[c] = sk;
+        if (k.zero) {
+            kp.wsat[c] = 0;                          // P == S_c at every wait
+        } else if (k1_key(k, 1ull << 33) != sk) {
+            kp.wsat[c] = ~0ull;
+        } else {
+            uint64_t lo = 0, hi = 1ull << 33;        // key(lo) != sk (lo = 0: P = S_c < cap), key(hi) == sk
+            while (hi - lo > 1) {
+                const uint64_t mid = lo + ((hi - lo) >> 1);
+                if (k1_key(k, mid) == sk) hi = mid;
+                else lo = mid;
+            }
+            kp.wsat[c] = hi;
+        }
     }
     kp.pad = 0;
     t.kpack[r] = kp;

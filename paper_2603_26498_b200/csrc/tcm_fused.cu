@@ -33,6 +33,9 @@ namespace tcm {
 namespace {
 
 constexpr uint32_t kThreads = 64;
+#ifndef TCM_FUSED_REUSEJ
+#define TCM_FUSED_REUSEJ 0
+#endif
 constexpr uint64_t kCalFpMask = (1ull << kCalCntShift) - 1;
 constexpr uint64_t kPending = 1ull << 63;
 
@@ -456,13 +459,20 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         if (stuck && st.n_dec > 0) {
             const uint64_t F = cal.next;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
-            uint64_t j = F - st.iter;
-            if (next_arr != ~0ull) {
-                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
-                j = ja < j ? ja : j;
+            uint64_t j = l4c_j;              // L4c's window is within the event / arrival / budget caps already
+#if TCM_FUSED_REUSEJ
+            if (l4c_j == ~0ull) {
+#else
+            {
+#endif
+                j = F - st.iter;
+                if (next_arr != ~0ull) {
+                    const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+                    j = ja < j ? ja : j;
+                }
+                j = j < budget ? j : budget;
+                j = j < l4c_j ? j : l4c_j;
             }
-            j = j < budget ? j : budget;
-            j = j < l4c_j ? j : l4c_j;
             st.clock += j * dt;
             st.iter += j;
             decided(j, st.n_pend);

@@ -53,8 +53,13 @@ struct __align__(16) ClassPack {
     uint32_t zero_mask;        // bit c: alpha * k_c == 0 (P == S_c)
     uint32_t filter_ok;        // FP32 bound validated for these constants (p <= 16, |C2| <= 1000)
     uint32_t pad;
+    // exact saturation: K1(w) == Smax for every w >= wsat[c] (K1 is non-decreasing in w and bounded by
+    // fl(S_c + 1), Lemma L1's premise), found by bisection at load within the audited [1, 2^33] us;
+    // satkey[c] = the key there.  wsat = ~0: no saturation inside that range.
+    uint64_t wsat[3];
+    uint64_t satkey[3];
 };
-static_assert(sizeof(ClassPack) == 144, "ClassPack layout");
+static_assert(sizeof(ClassPack) == 192, "ClassPack layout");
 
 // Model constants in the kernels' parameter space.
 struct ModelConst {

@@ -51,6 +51,9 @@ constexpr uint8_t RS_DEC = 32, RS_PREV = 64, RS_GEN = 128;
 #ifndef TCM_SW_STAGES
 #define TCM_SW_STAGES 4
 #endif
+#ifndef TCM_SW_SAT
+#define TCM_SW_SAT 1
+#endif
 #ifndef TCM_SW_MINB
 #define TCM_SW_MINB 3
 #endif
@@ -625,10 +628,10 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
       for (int kit = 0; kit < kItersPerLaunch; ++kit) {
         // the replica's class pack, parameters and offset do not depend on its state: load them
         // before the prologue so their latency overlaps the state load
-        if (wl == 0 && kit == 0) {   // stage the replica's ClassPack (144 B) in this CTA's shared memory
-            const uint32_t* src = reinterpret_cast<const uint32_t*>(t.kpack + r);
-            uint32_t* dst = reinterpret_cast<uint32_t*>(&sm.kp);
-            for (int q = lane; q < (int)(sizeof(ClassPack) / 4); q += 32) dst[q] = src[q];
+        if (wl == 0 && kit == 0) {   // stage the replica's ClassPack (192 B) in this CTA's shared memory
+            static_assert(sizeof(ClassPack) % 16 == 0 && sizeof(ClassPack) / 16 <= 32, "one 16-byte load per lane");
+            if (lane < (int)(sizeof(ClassPack) / 16))
+                reinterpret_cast<uint4*>(&sm.kp)[lane] = __ldg(reinterpret_cast<const uint4*>(t.kpack + r) + lane);
         }
         const tcm_replica_params prm = t.params[r];
         const uint64_t base = t.offset[r];
@@ -834,8 +837,15 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 if (!__any_sync(0xFFFFFFFFu, live)) return;
                 if (live) {
                     const int c = cc & RS_CLS;
+#if TCM_SW_SAT
+                    // a wait past the class's saturation point has the cap's key exactly (ClassPack.wsat)
+                    key = prio ? (qwl >= sm.kp.wsat[c] ? sm.kp.satkey[c]
+                                                       : k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qwl, tb))
+                               : (edf ? ~(clock - qwl) : 0);     // EDF: ~(deadline x den); FCFS / aging: 0
+#else
                     key = prio ? k1_key_bf(sm.kp.S[c], sm.kp.p[c], sm.kp.C[c], (zero_mask >> c) & 1u, qwl, tb)
                                : (edf ? ~(clock - qwl) : 0);     // EDF: ~(deadline x den); FCFS / aging: 0
+#endif
                     if (first_pass && (cc & RS_RES)) {                 // partial: remember its key
                         const int slot = atomicAdd(&gsm.npart, 1);
                         if (slot < kMaxPart) {
@@ -1069,6 +1079,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 const int lastl = nvalid > 0 ? (int)nvalid - 1 : 0;
                 const uint64_t lastk = __shfl_sync(0xFFFFFFFFu, lk, lastl);
                 const uint32_t lasti = __shfl_sync(0xFFFFFFFFu, li, lastl);
+                __syncwarp();            // every lane's reads of the group state precede lane 0's writes
                 if (lane == 0) {
                     gsm.st.seq += __popc(adm_mask);
                     gsm.st.kv_free = kv - sum_f;
@@ -1119,6 +1130,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                         }
                         __syncwarp();
                     }
+                    __syncwarp();
                     if (lane == 0) gsm.pass_more = 0;
                 }
             }
@@ -1220,6 +1232,7 @@ __global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, Tr
                 }
                 l2 += 32;
             }
+            __syncwarp();
             if (lane == 0) {
                 st.kv_free += kv_add;
                 st.n_dec += (uint32_t)n_dec_add;

@@ -10,6 +10,8 @@ from paper_2603_26498_b200 import tcm
 
 mode = sys.argv[1]
 R, n = (8, 300) if mode != "cluster" else (1, 3000)
+if len(sys.argv) > 3:
+    R, n = int(sys.argv[2]), int(sys.argv[3])
 growth = mode in ("growth", "edf")
 kv = 16384
 reps = np.array([T.make_replica(7, r, n, 4.0, (0.5, 0.2, 0.3), kv - 2048 if growth else kv) for r in range(R)])
