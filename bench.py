@@ -453,9 +453,9 @@ def run_tcm(args, rank, world, local):
         out["roofline_step"] = st_res.pop("C2'")
         out["step_kernels"] = st_res
 
-    if not args.skip_next1 and rank == 0:
-        out["next1"] = bench_next1(args, dev, stream)
-        log("next1 done")
+    if not args.skip_next1 and rank == 0:          # fig:preemptions with all three policies (stepwise)
+        out["next1_policies"] = bench_next1(args, dev, stream)
+        log("next1 (stepwise, FCFS/EDF/TCM) done")
 
     # end-to-end through the C ABI with HOST buffers (H2D + run + D2H inside the timed region)
     log("stepwise done")
@@ -474,6 +474,16 @@ def run_tcm(args, rank, world, local):
         out["e2e"] = bench_e2e(args, sw, host, dev, dist, world, (pick.cpu().numpy(), ref))
         del host
     log("e2e done")
+
+    if not args.skip_next1 and args.workload == "c4" and rank == 0:
+        # NEXT-1 at the C4 size (65,536 x 10,000) on the fused engine (k_fgrow), after the
+        # device-resident C4 run is freed
+        sim.close()
+        trace = results = None
+        torch.cuda.empty_cache()
+        out["next1"] = bench_next1(args, dev, stream, engine=tcm.ENGINE_FUSED, replicas=args.replicas,
+                                   requests=args.requests, policies=(tcm.POLICY_FCFS, tcm.POLICY_TCM))
+        log("next1 (fused, C4 size) done")
 
     if rank == 0 and world == 1 and not args.skip_cpu:      # the oracle baseline: rank 0 at N=1 only
         s = oracle_sample(sw, n_trunc=0 if args.cpu_full else args.ref_requests,
@@ -614,23 +624,29 @@ def c2_latency(sim, stream, reps, flush, dev):
             "kernel_p90_us": float(np.percentile(ks, 90)) * 1e3, "pending": pend}
 
 
-def bench_next1(args, dev, stream):
-    """NEXT-1 (decode KV growth + preemption by recomputation, R28-R32) on the stepwise engine:
-    the C4 cells with tcm.KV_GROWTH at a reduced size; simulated requests/s, preemptions and the
-    motorcycle share of the victims per policy (fig:preemptions)."""
+def bench_next1(args, dev, stream, engine=None, replicas=None, requests=None, policies=None, reps=2):
+    """NEXT-1 (decode KV growth + preemption by recomputation, R28-R32): the C4 grid with
+    tcm.KV_GROWTH; simulated requests/s, preemptions and, per policy, the class of the victims and
+    the time spent preempted (fig:preemptions).  Default: the stepwise engine at
+    a reduced size with FCFS, EDF (R34 inversion preemption) and TCM cells; engine=FUSED runs k_fgrow
+    (FCFS and TCM: EDF is not class-monotone)."""
     import torch
     from paper_2603_26498_b200 import tcm
     from paper_2603_26498_b200 import workloads as W
-    sw = W.c4_growth(replicas_per_gpu=args.next1_replicas, n_requests=args.next1_requests)
+    engine = tcm.ENGINE_STEPWISE if engine is None else engine
+    replicas = replicas or args.next1_replicas
+    requests = requests or args.next1_requests
+    policies = policies or (tcm.POLICY_FCFS, tcm.POLICY_TCM, tcm.POLICY_EDF)
+    sw = W.c4_growth(replicas_per_gpu=replicas, n_requests=requests, policies=policies)
     with torch.cuda.stream(stream):
         tr = tcm.generate_device(sw.gen, device=dev, stream=stream)
         tr["params"] = torch.from_numpy(sw.params.view(np.uint8)).to(dev)
         res = tcm.alloc_results(sw.n_requests, device=dev, preemption=True)
     stream.synchronize()
-    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE, n_cells=sw.n_cells), stream)
+    sim = tcm.Simulation(tcm.config(engine=engine, n_cells=sw.n_cells), stream)
     sim.load(tr, res)
     times = []
-    for rep in range(2):                       # the first run is warm-up
+    for rep in range(reps):                    # the first run is warm-up
         sim.reset()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -646,19 +662,22 @@ def bench_next1(args, dev, stream):
     cell_pol = np.array([c["policy"] for c in sw.cells])
     by = {}
     for name, p in (("FCFS", tcm.POLICY_FCFS), ("EDF", tcm.POLICY_EDF), ("TCM", tcm.POLICY_TCM)):
+        if p not in policies:
+            continue
         summ = M.preemption_summary(pst[cell_pol == p])
         by[name] = {"preemptions": summ["all"]["preemptions"], "motorcycle_preemptions": summ["M"]["preemptions"],
                     "requests_preempted": summ["all"]["requests_preempted"],
                     "preempted_s": {g: round(summ[g]["preempted_s"], 3) for g in ("M", "C", "T")}}
     sim.close()
-    return {"workload": f"C4-growth: {sw.n_replicas} replicas x {args.next1_requests} requests (C4 cells, "
-                        "KV growth + preemption; FCFS, EDF with R34 inversion preemption, TCM), stepwise engine",
+    names = "/".join({tcm.POLICY_FCFS: "FCFS", tcm.POLICY_TCM: "TCM", tcm.POLICY_EDF: "EDF"}[p] for p in policies)
+    eng = "fused engine (k_fgrow)" if engine == tcm.ENGINE_FUSED else "stepwise engine"
+    return {"workload": f"C4-growth: {sw.n_replicas} replicas x {requests} requests (C4 grid x {names}, "
+                        f"KV growth + preemption by recomputation), {eng}",
             "value": sw.n_requests / (ms / 1e3), "unit": "requests/s", "ms": ms,
             "decisions_per_s": st["decisions"] / (ms / 1e3), "iterations": st["iterations"],
+            "scanned_decisions": st["scanned_decisions"],
             "preemptions": st["preemptions"], "forced_preemptions": st["forced_preemptions"],
-            "by_policy": by,
-            "note": "bounded by the heaviest replica's serial iteration chain (no closed-form fast-forward "
-                    "under KV growth); DESIGN.md 9"}
+            "by_policy": by}
 
 
 def host_copy(trace):

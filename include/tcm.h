@@ -73,7 +73,8 @@ enum { TCM_POLICY_FCFS = 0, TCM_POLICY_TCM = 1, TCM_POLICY_EDF = 2, TCM_POLICY_N
                                tokens, victims are preempted (FCFS/EDF/naive aging: most recently
                                arrived; TCM: lowest-ranked non-motorcycle) and re-prefill what
                                they held.  Needs footprint + out - 1 <= kv_capacity for every
-                               request (else TCM_E_CAPACITY).  STEPWISE only.                */
+                               request (else TCM_E_CAPACITY).  Both engines (FUSED: k_fgrow,
+                               DESIGN.md 6.5; with EDF: STEPWISE only).                       */
 
 enum { TCM_ENGINE_FUSED = 0, TCM_ENGINE_STEPWISE = 1 };
 /* Development knobs read from the environment at each run (not part of the contract; results are
@@ -82,7 +83,9 @@ enum { TCM_ENGINE_FUSED = 0, TCM_ENGINE_STEPWISE = 1 };
  * per warp. */
 /* FUSED   : one persistent thread per replica runs the whole step loop in registers;
  *           a3 is the exact 3-way merge of the class-FIFO heads (Lemma L1).
- *           Replicas must hold < 2^24 requests (calendar slot counters).
+ *           Replicas must hold < 2^24 requests (calendar slot counters).  TCM_KV_GROWTH
+ *           replicas run in k_fgrow (preempted requests re-enter their class queue in front)
+ *           and need about 33 B more workspace per request than tcm_workspace_bytes reports.
  * STEPWISE: the paper-literal step -- per iteration, every pending request of every
  *           active replica is re-keyed (a1+a2), top-k selected (a3), prefix-scanned (a4),
  *           then the clock kernel runs (a5).  Bit-identical results; used for the

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -42,7 +43,10 @@ struct tcm_ctx {
     struct Graph { uint32_t iters; cudaGraphExec_t exec; uint64_t launches; bool deferred; };
     std::vector<Graph> graphs;
     std::vector<uint32_t> graph_seen;
+    std::vector<uint32_t> graph_never;   // n whose capture failed: always eager
     uint32_t* h_active = nullptr;        // pinned: the graphs' copy target
+    cudaStream_t cs = nullptr;           // capture stream (the caller's may be the legacy stream,
+                                         // which cannot be captured; a graph launches into any stream)
 };
 
 namespace {
@@ -84,6 +88,7 @@ void free_allocs(tcm_ctx* c, bool keep = false) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);   // they captured the old trace's pointers
     c->graphs.clear();
     c->graph_seen.clear();
+    c->graph_never.clear();
 }
 
 tcm_status dalloc(tcm_ctx* c, void** p, size_t bytes) {
@@ -209,6 +214,11 @@ tcm_status reset_state(tcm_ctx* c) {
     if (t.pcount) TCM_CUDA(c, cudaMemsetAsync(t.pcount, 0, 4 * (N ? N : 1), s));
     if (t.ptime) TCM_CUDA(c, cudaMemsetAsync(t.ptime, 0, 8 * (N ? N : 1), s));
     if (t.genp) TCM_CUDA(c, cudaMemsetAsync(t.genp, 0, 4 * (N ? N : 1), s));
+    if (t.fg.pfin) {
+        const uint64_t P = N + 6ull * R;
+        TCM_CUDA(c, cudaMemsetAsync(t.fg.pfin, 0, 8 * P, s));
+        TCM_CUDA(c, cudaMemsetAsync(t.fg.pflag, 0, P, s));
+    }
     launch_init(t, s);
     c->launches++;
     if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
@@ -227,25 +237,27 @@ tcm_status reset_state(tcm_ctx* c) {
 constexpr uint32_t kGraphMaxIters = 64;
 
 // Everything one engine call enqueues, ending with the active-count copy to `active_dst`.
-tcm_status enqueue_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active_dst, uint64_t* launches, bool* deferred) {
+// timed = false (graph capture): no event records -- events recorded by graph nodes cannot be timed
+tcm_status enqueue_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active_dst, uint64_t* launches, bool* deferred,
+                          bool timed = true) {
     *deferred = false;
     if (c->cfg.engine == TCM_ENGINE_FUSED) TCM_CUDA(c, cudaMemsetAsync(c->d_active, 0, 4, c->s));
-    TCM_CUDA(c, cudaEventRecord(c->ev[2], c->s));
+    if (timed) TCM_CUDA(c, cudaEventRecord(c->ev[2], c->s));
     if (c->cfg.engine == TCM_ENGINE_FUSED) {
         launch_fused(c->m, c->t, max_iters, c->d_active, c->s);
-        TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
+        if (timed) TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
         launch_fused_stamp(c->t, c->s);
         *launches += 2;
     } else {
         double kms = 0;
-        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, launches, c->ev[5], c->ev[6],
-                                     &kms, deferred);
+        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, launches,
+                                     timed ? c->ev[5] : nullptr, timed ? c->ev[6] : nullptr, &kms, deferred);
         c->engine_ms += kms;
         if (st != TCM_OK) return fail(c, st, "stepwise engine failed: %s", cudaGetErrorString(cudaGetLastError()));
     }
     TCM_CUDA(c, cudaGetLastError());
-    if (c->cfg.engine != TCM_ENGINE_FUSED) TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
-    TCM_CUDA(c, cudaEventRecord(c->ev[4], c->s));
+    if (timed && c->cfg.engine != TCM_ENGINE_FUSED) TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
+    if (timed) TCM_CUDA(c, cudaEventRecord(c->ev[4], c->s));
     TCM_CUDA(c, cudaMemcpyAsync(active_dst, c->d_active, 4, cudaMemcpyDeviceToHost, c->s));
     return TCM_OK;
 }
@@ -253,6 +265,8 @@ tcm_status enqueue_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active_dst, 
 // The graph of a short call (max_iters <= kGraphMaxIters, one k_step chunk), or nullptr.
 const tcm_ctx::Graph* step_graph(tcm_ctx* c, uint32_t max_iters) {
     if (max_iters > kGraphMaxIters || !c->h_active) return nullptr;
+    if (const char* g = getenv("TCM_GRAPHS"))                 // development knob: "0" = always eager
+        if (g[0] == '0') return nullptr;
     for (auto& g : c->graphs)
         if (g.iters == max_iters) return &g;
     bool seen = false;
@@ -261,22 +275,36 @@ const tcm_ctx::Graph* step_graph(tcm_ctx* c, uint32_t max_iters) {
         c->graph_seen.push_back(max_iters);
         return nullptr;
     }
+    for (uint32_t k : c->graph_never)
+        if (k == max_iters) return nullptr;
     cudaGraph_t graph = nullptr;
     uint64_t l = 0;
     bool deferred = false;
-    if (cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return nullptr;
-    tcm_status st = enqueue_engine(c, max_iters, c->h_active, &l, &deferred);
-    cudaError_t e = cudaStreamEndCapture(c->s, &graph);
-    if (st != TCM_OK || e != cudaSuccess || !graph || !deferred) {
-        if (graph) cudaGraphDestroy(graph);
+    const std::string err0 = c->err;
+    if (!c->cs && cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking) != cudaSuccess) {
+        c->cs = nullptr;
         cudaGetLastError();
         return nullptr;
     }
+    cudaStream_t user = c->s;
+    c->s = c->cs;
+    cudaError_t e = cudaStreamBeginCapture(c->s, cudaStreamCaptureModeRelaxed);
+    tcm_status st = e == cudaSuccess ? enqueue_engine(c, max_iters, c->h_active, &l, &deferred, false) : TCM_E_CUDA;
+    const cudaError_t ecap = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamEndCapture(c->s, &graph);
+    c->s = user;
     cudaGraphExec_t exec = nullptr;
-    e = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) {
+    cudaError_t einst = cudaSuccess;
+    const bool one_chunk = c->cfg.engine == TCM_ENGINE_FUSED || deferred;   // stepwise: no mid-call synchronisation
+    if (st == TCM_OK && e == cudaSuccess && graph && one_chunk) einst = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (st != TCM_OK || e != cudaSuccess || !one_chunk || einst != cudaSuccess || !exec) {
+        if (getenv("TCM_GRAPH_DEBUG"))
+            fprintf(stderr, "libtcm: no graph for tcm_step(%u): status %d, capture %s / %s, instantiate %s\n", max_iters,
+                    (int)st, cudaGetErrorString(ecap), cudaGetErrorString(e), cudaGetErrorString(einst));
         cudaGetLastError();
+        c->err = err0;                             // the eager path below is the call's result
+        c->graph_never.push_back(max_iters);
         return nullptr;
     }
     c->graphs.push_back({max_iters, exec, l, deferred});
@@ -285,7 +313,10 @@ const tcm_ctx::Graph* step_graph(tcm_ctx* c, uint32_t max_iters) {
 
 tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
     if (const tcm_ctx::Graph* g = step_graph(c, max_iters)) {
+        // engine_ms of a replayed call is the whole graph (its launches and the active-count copy)
+        TCM_CUDA(c, cudaEventRecord(c->ev[2], c->s));
         TCM_CUDA(c, cudaGraphLaunch(g->exec, c->s));
+        TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
         TCM_CUDA(c, cudaStreamSynchronize(c->s));
         *active = *c->h_active;
         c->launches += g->launches;
@@ -295,11 +326,8 @@ tcm_status run_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active) {
             c->reset_ms += ms;
             c->reset_pending = false;
         }
-        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->cfg.engine == TCM_ENGINE_FUSED ? c->ev[2] : c->ev[5],
-                                         c->cfg.engine == TCM_ENGINE_FUSED ? c->ev[3] : c->ev[6]));
+        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
         c->engine_ms += ms;
-        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
-        c->stamp_ms += ms;
         return TCM_OK;
     }
     bool deferred = false;      // stepwise: k_step events still to be read after the sync below
@@ -485,8 +513,38 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     TCM_CUDA(c, cudaGetLastError());
     TCM_CUDA(c, cudaMemcpyAsync(hv, c->d_val, 12, cudaMemcpyDeviceToHost, s));
     TCM_CUDA(c, cudaStreamSynchronize(s));
-    c->t.any_growth = hv[2];
-    t.any_growth = hv[2];
+    c->t.any_growth = t.any_growth = hv[2] & 1u;
+    c->t.all_growth = t.all_growth = (hv[2] & 2u) == 0;
+    if (c->cfg.engine == TCM_ENGINE_FUSED && t.any_growth && hv[0] == ST_OK) {
+        // NEXT-1 on the fused engine (k_fgrow): per-position state, per-class stacks, preemption results
+        const uint64_t P = N + 6ull * R;
+        if ((st = dalloc(c, &p, 8 * P))) return st;
+        t.fg.pfin = (uint64_t*)p;
+        if ((st = dalloc(c, &p, 4 * P))) return st;
+        t.fg.pkv = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 4 * P))) return st;
+        t.fg.prem = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 4 * P))) return st;
+        t.fg.pgen = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 4 * P))) return st;
+        t.fg.pnext = (uint32_t*)p;
+        if ((st = dalloc(c, &p, P))) return st;
+        t.fg.pflag = (uint8_t*)p;
+        if ((st = dalloc(c, &p, 12ull * R))) return st;
+        t.fg.top = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 12ull * R))) return st;
+        t.fg.seg = (uint32_t*)p;
+        if ((st = dalloc(c, &p, 12ull * R))) return st;
+        t.fg.hres = (uint32_t*)p;
+        const uint64_t Nn = N ? N : 1;
+        if ((st = dalloc(c, &p, 8 * Nn))) return st;
+        t.pstart = (uint64_t*)p;
+        if (dev_res && rv->preempt_count) t.pcount = rv->preempt_count;
+        else { if ((st = dalloc(c, &p, 4 * Nn))) return st; t.pcount = (uint32_t*)p; }
+        if (dev_res && rv->preempted_us) t.ptime = rv->preempted_us;
+        else { if ((st = dalloc(c, &p, 8 * Nn))) return st; t.ptime = (uint64_t*)p; }
+        c->t = t;
+    }
     if (hv[0] == ST_CAPACITY)
         return fail(c, TCM_E_CAPACITY, "replica %u: a footprint (with TCM_KV_GROWTH: footprint + out - 1) exceeds kv_capacity (R18, R28)", hv[1]);
     if (hv[0] != ST_OK)
@@ -631,6 +689,7 @@ void tcm_destroy(tcm_ctx* c) {
     cudaFree(c->d_acc);
     cudaFree(c->d_val);
     if (c->h_active) cudaFreeHost(c->h_active);
+    if (c->cs) cudaStreamDestroy(c->cs);
     delete c;
 }
 

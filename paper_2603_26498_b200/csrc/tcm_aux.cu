@@ -96,8 +96,9 @@ __global__ void k_validate(TraceDev t, uint32_t* v, int general_ok) {
     if (p.policy > TCM_POLICY_NAIVE_AGING || p.chunk_budget == 0 || p.kv_capacity == 0 ||
         p.kv_capacity > 0xFFFFFFFFull || !(p.aging_alpha >= 0.0) || (p.flags & ~(TCM_ADMIT_SKIP | TCM_KV_GROWTH)) != 0)
         bad = ST_BAD_INPUT;
-    // EDF and first-fit admission break Lemmas L1/L2: only the stepwise engine runs them
-    if (!general_ok && (p.policy == TCM_POLICY_EDF || (p.flags & (TCM_ADMIT_SKIP | TCM_KV_GROWTH)))) bad = ST_BAD_INPUT;
+    // EDF and first-fit admission break Lemmas L1/L2: only the stepwise engine runs them (TCM_KV_GROWTH
+    // runs on both: the fused engine's k_fgrow)
+    if (!general_ok && (p.policy == TCM_POLICY_EDF || (p.flags & TCM_ADMIT_SKIP))) bad = ST_BAD_INPUT;
     const bool growth = (p.flags & TCM_KV_GROWTH) != 0;
     // fused calendar slots count finishing requests in 24 bits
     if (!general_ok && b - a >= (1ull << (64 - kCalCntShift))) bad = ST_BAD_INPUT;
@@ -112,7 +113,7 @@ __global__ void k_validate(TraceDev t, uint32_t* v, int general_ok) {
         }
     }
     // ST_BAD_INPUT (2) vs ST_CAPACITY (3): report the larger code
-    if (lane == 0 && growth) atomicOr(&v[2], 1u);
+    if (lane == 0) atomicOr(&v[2], growth ? 1u : 2u);      // bit 0: some replica grows; bit 1: some does not
     const uint32_t worst = __reduce_max_sync(0xFFFFFFFFu, bad);
     if (lane == 0 && worst != ST_OK) {
         atomicMax(&v[0], worst);

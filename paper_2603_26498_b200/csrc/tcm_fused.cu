@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "tcm_fcal.cuh"
 #include "tcm_internal.cuh"
 #include "tcm_k1.cuh"
 
@@ -32,174 +33,10 @@ namespace tcm {
 
 namespace {
 
-constexpr uint32_t kThreads = 64;
+constexpr uint32_t kThreads = kFThreads;
 #ifndef TCM_FUSED_REUSEJ
 #define TCM_FUSED_REUSEJ 0
 #endif
-constexpr uint64_t kCalFpMask = (1ull << kCalCntShift) - 1;
-constexpr uint64_t kPending = 1ull << 63;
-
-__device__ __forceinline__ void ld_rec(const FRec* p, uint64_t& arr, uint32_t& f, uint32_t& inl, uint32_t& id,
-                                       uint32_t& out) {
-    uint64_t a, b, c, d;
-    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
-    arr = a;
-    f = (uint32_t)b;
-    inl = (uint32_t)(b >> 32);
-    id = (uint32_t)c;
-    out = (uint32_t)(c >> 32);
-}
-
-// (arrival, footprint) of a record
-__device__ __forceinline__ void ld_arrfp(const FRec* p, uint64_t& arr, uint32_t& f) {
-    uint64_t a, b;
-    asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
-    arr = a;
-    f = (uint32_t)b;
-}
-// Asynchronous 16-byte copy global -> shared (its own commit group).  `dep` is an unused operand
-// that makes the copy wait for a register (the value just read from the same shared slot).
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t dep) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("{\n\t.reg .b64 d;\n\tmov.b64 d, %2;\n\tcp.async.cg.shared.global [%0], [%1], 16;\n\t"
-                 "cp.async.commit_group;\n\t}" ::"r"(sa), "l"(gmem), "l"(dep) : "memory");
-}
-// Wait until at most `newer` of this thread's most recent copy groups are still in flight.
-__device__ __forceinline__ void cp_async_wait(uint32_t newer) {
-    if (newer == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-    else if (newer == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else if (newer == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-    else asm volatile("cp.async.wait_group 3;" ::: "memory");
-}
-
-// (inline, id, out) of a record, usually an L1 hit: its sector came in with ld_arrfp
-__device__ __forceinline__ void ld_inl_id_out(const FRec* p, uint32_t& inl, uint32_t& id, uint32_t& out) {
-    uint32_t f;
-    asm("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-        : "=r"(f), "=r"(inl), "=r"(id), "=r"(out) : "l"(reinterpret_cast<const char*>(p) + 8));
-}
-
-__device__ __forceinline__ void red_add(uint64_t* p, uint64_t v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ uint64_t rotr64(uint64_t x, uint32_t k) {
-    k &= 63;
-    return k ? (x >> k) | (x << (64 - k)) : x;
-}
-
-// Calendar occupancy: bit (slot & 31) of word (slot >> 5) in shared memory (column = thread),
-// and `sum` bit w set iff word w is non-zero.
-struct Occ {
-    uint32_t (*w)[kThreads];
-    uint32_t tid;
-    __device__ __forceinline__ uint32_t& word(uint32_t i) const { return w[i][tid]; }
-};
-
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// The decode calendar of one replica.  Slot F & 2047 counts the requests whose last decode
-// token comes in iteration F: (count << 40) | sum of their footprints.  The slot of the next
-// event `next` is held in registers: `pre` (its memory value, loaded as soon as it becomes
-// the next event, so the load overlaps the iterations before it) plus `add` (insertions into
-// it since); other insertions go to memory as fire-and-forget reductions.
-struct Calendar {
-    uint64_t* cal;
-    Occ occ;
-    uint64_t sum;     // bit w: occupancy word w non-zero
-    uint64_t next;    // iteration of the next event (~0: none)
-    uint64_t pre, add;
-
-    // Iteration of the next occupied slot after `iter` (one exists when n_dec > 0).
-    __device__ __forceinline__ uint64_t scan(uint64_t iter) const {
-        const uint32_t s0 = (uint32_t)((iter + 1) & (kCalSlots - 1));
-        const uint32_t wi = s0 >> 5;
-        uint32_t wv = occ.word(wi) & (~0u << (s0 & 31));
-        uint32_t word = wi;
-        if (wv == 0) {
-            const uint64_t rr = rotr64(sum, wi + 1);      // bit k: word (wi + 1 + k) mod 64
-            word = (wi + 1 + (uint32_t)(__ffsll((long long)rr) - 1)) & (kCalWords - 1);
-            wv = occ.word(word);
-            if (word == wi) wv &= ~(~0u << (s0 & 31));    // wrapped round to slots before s0
-        }
-        const uint32_t slot = word * 32 + (uint32_t)(__ffs(wv) - 1);
-        return iter + 1 + (uint64_t)((slot - s0) & (kCalSlots - 1));
-    }
-    __device__ __forceinline__ void find_next(uint64_t iter, uint32_t n_dec) {
-        add = 0;
-        if (n_dec > 0) {
-            next = scan(iter);
-            pre = ld_relaxed(cal + (next & (kCalSlots - 1)));
-        } else {
-            next = ~0ull;
-            pre = 0;
-        }
-    }
-    // A request of footprint f whose last token comes in iteration F (> the current one).
-    __device__ __forceinline__ void insert(uint64_t F, uint32_t f) {
-        const uint64_t v = (1ull << kCalCntShift) | f;
-        const uint32_t s = (uint32_t)(F & (kCalSlots - 1));
-        occ.word(s >> 5) |= 1u << (s & 31);
-        sum |= 1ull << (s >> 5);
-        if (F == next) {
-            add += v;
-        } else if (F < next) {                         // F becomes the next event; slot F is empty
-            if (add) red_add(cal + (next & (kCalSlots - 1)), add);
-            next = F;
-            pre = 0;
-            add = v;
-        } else {
-            red_add(cal + s, v);
-        }
-    }
-    // Step 9 for iteration `next`: every request whose last decode token is
-    // produced now completes and releases its KV (R7).  k_fstamp stamps their done_us from the
-    // event log.
-    __device__ __forceinline__ void process(ReplicaState& st) {
-        const uint32_t s = (uint32_t)(next & (kCalSlots - 1));
-        const uint64_t v = pre + add;
-        if (pre) st_relaxed(cal + s, 0);
-        const uint32_t cnt = (uint32_t)(v >> kCalCntShift);
-        st.kv_free += v & kCalFpMask;
-        st.n_dec -= cnt;
-        uint32_t& w = occ.word(s >> 5);
-        w &= ~(1u << (s & 31));
-        if (w == 0) sum &= ~(1ull << (s >> 5));
-        find_next(st.iter, st.n_dec);
-    }
-    __device__ __forceinline__ void flush() {
-        if (add) red_add(cal + (next & (kCalSlots - 1)), add);
-    }
-};
-
-// One (iteration, clock) entry of the replica's event log: iterations in which a prefill
-// completed or a decode finished, strictly increasing (k_fstamp looks them up).
-__device__ __forceinline__ void log_event(uint64_t* log, ReplicaState& st) {
-    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(log + 2 * (uint64_t)st.nlog), "l"(st.iter),
-                 "l"(st.clock) : "memory");
-    st.nlog++;
-}
-
-template <class T>
-__device__ __forceinline__ T sel3(int i, const T (&a)[3]) {
-    return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
-}
-
-// Exact K1 key of class c after waiting w, from the replica's class constants.  Out of line:
-// the scan needs it only for heads whose FP32 bounds are within 2.5e-4, and one copy keeps the
-// loop's code small.
-__device__ __noinline__ uint64_t exact_key(const ClassPack* kp, int c, uint64_t w) {
-    const K1Class kc{__ldg(&kp->S[c]), __ldg(&kp->p[c]), __ldg(&kp->C[c]), ((__ldg(&kp->zero_mask) >> c) & 1u) != 0};
-    return k1_key(kc, w);
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
@@ -253,6 +90,11 @@ __global__ void k_fpack(ModelConst m, TraceDev t) {
         st.head[1] = cnt0 + 2;
         st.head[2] = cnt0 + cnt1 + 4;
     }
+    if (t.fg.top && lane < 3) {           // NEXT-1 (k_fgrow): empty preempted stacks, segment starts
+        t.fg.top[3 * r + lane] = NIL;
+        t.fg.seg[3 * r + lane] = lane == 0 ? 0 : (lane == 1 ? cnt0 + 2 : cnt0 + cnt1 + 4);
+        t.fg.hres[3 * r + lane] = 0;
+    }
 }
 
 // lpw: replicas per warp (a power of two <= 32).  With fewer replicas than resident lanes the warps
@@ -267,6 +109,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     if ((gthread & 31) >= lpw) return;
     const uint32_t r = (gthread >> 5) * lpw + (gthread & 31);
     if (r >= t.R) return;
+    if (t.fg.top && (t.params[r].flags & TCM_KV_GROWTH)) return;   // k_fgrow runs the NEXT-1 replicas
     ReplicaState st = t.state[r];
     if (st.flags & FLAG_FINISHED) return;
     const uint32_t tid = threadIdx.x;
@@ -459,20 +302,25 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         if (stuck && st.n_dec > 0) {
             const uint64_t F = cal.next;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
-            uint64_t j = l4c_j;              // L4c's window is within the event / arrival / budget caps already
 #if TCM_FUSED_REUSEJ
+            uint64_t j = l4c_j;              // L4c's window is within the event / arrival / budget caps already
             if (l4c_j == ~0ull) {
-#else
-            {
-#endif
                 j = F - st.iter;
                 if (next_arr != ~0ull) {
                     const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                     j = ja < j ? ja : j;
                 }
                 j = j < budget ? j : budget;
-                j = j < l4c_j ? j : l4c_j;
             }
+#else
+            uint64_t j = F - st.iter;
+            if (next_arr != ~0ull) {
+                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+                j = ja < j ? ja : j;
+            }
+            j = j < budget ? j : budget;
+            j = j < l4c_j ? j : l4c_j;
+#endif
             st.clock += j * dt;
             st.iter += j;
             decided(j, st.n_pend);
@@ -810,6 +658,9 @@ void launch_fused_prologue(const ModelConst& m, const TraceDev& t, cudaStream_t 
     k_fpack<<<(uint32_t)blocks, threads, 0, s>>>(m, t);
 }
 
+void launch_fgrow(const ModelConst& m, const TraceDev& t, uint32_t max_iters, uint32_t* d_active, uint32_t lpw,
+                  cudaStream_t s);
+
 void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, uint32_t* d_active,
                   cudaStream_t s) {
     // replicas per warp: the smallest power of two that keeps every replica in the resident warps
@@ -834,7 +685,8 @@ void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, ui
     }
     const uint64_t nwarps = ((uint64_t)t.R + lpw - 1) / lpw;
     const uint32_t blocks = (uint32_t)((nwarps * 32 + kThreads - 1) / kThreads);
-    k_fused<<<blocks, kThreads, 0, s>>>(m, t, max_iters, d_active, lpw);
+    if (!t.all_growth) k_fused<<<blocks, kThreads, 0, s>>>(m, t, max_iters, d_active, lpw);
+    if (t.any_growth) launch_fgrow(m, t, max_iters, d_active, lpw, s);
 }
 
 void launch_fused_stamp(const TraceDev& t, cudaStream_t s) {

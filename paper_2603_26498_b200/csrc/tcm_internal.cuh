@@ -93,6 +93,20 @@ struct FusedWs {
 };
 constexpr int kCalCntShift = 40;
 
+// Fused engine under TCM_KV_GROWTH (NEXT-1, k_fgrow): state per class-segment position
+// (the FRec index: replica r's positions start at offset[r] + 6r), and per replica and class.
+struct FGrowWs {
+    uint64_t* pfin;          // [N + 6R] finish iteration of the request decoding at this position (0: not decoding)
+    uint32_t* pkv;           // [N + 6R] KV it holds at that finish (released there)
+    uint32_t* prem;          // [N + 6R] waiting victim: KV to reserve = tokens to re-prefill (R30)
+    uint32_t* pgen;          // [N + 6R] tokens generated so far (set at admission / preemption)
+    uint32_t* pnext;         // [N + 6R] preempted-stack link
+    uint8_t* pflag;          // [N + 6R] bit 0: first token emitted; bit 1: admitted before
+    uint32_t* top;           // [R * 3] per class: top of the preempted stack (NIL: empty)
+    uint32_t* seg;           // [R * 3] per class: first position of the class segment
+    uint32_t* hres;          // [R * 3] per class: KV reserved by the class head while it is reserved
+};
+
 // Everything a kernel needs about the bound trace (device pointers).
 struct TraceDev {
     uint32_t R;
@@ -124,7 +138,9 @@ struct TraceDev {
     uint32_t* pcount;        // [N] preemptions (result)
     uint64_t* ptime;         // [N] preempted time (result)
     uint32_t any_growth;     // some replica sets TCM_KV_GROWTH (from k_validate)
+    uint32_t all_growth;     // every replica does
     FusedWs fw;              // fused engine only
+    FGrowWs fg;              // fused engine with some TCM_KV_GROWTH replica only
 };
 
 __device__ __forceinline__ int classify(const ModelConst& m, uint32_t mod, uint32_t f) {

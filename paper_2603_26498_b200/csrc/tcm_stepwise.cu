@@ -1391,7 +1391,7 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         if ((uint64_t)max_iters - done_launches < this_chunk) this_chunk = (uint32_t)(max_iters - done_launches);
         if (done_launches > 0 && cudaMemsetAsync(d_active, 0, 4, s) != cudaSuccess) return TCM_E_CUDA;
         // device time of the k_step launches alone (tcm_stats_host.engine_ms)
-        if (cudaEventRecord(ev_begin, s) != cudaSuccess) return TCM_E_CUDA;
+        if (ev_begin && cudaEventRecord(ev_begin, s) != cudaSuccess) return TCM_E_CUDA;   // null: untimed (graph capture)
         for (uint32_t q = 0; q < this_chunk; ++q) {
             const int last = q + 1 == this_chunk;
             if (L.cluster > 1) {
@@ -1422,7 +1422,7 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
             ctr_base += per_launch;
         }
         done_launches += this_chunk;
-        if (cudaEventRecord(ev_end, s) != cudaSuccess) return TCM_E_CUDA;
+        if (ev_end && cudaEventRecord(ev_end, s) != cudaSuccess) return TCM_E_CUDA;
         if (cudaGetLastError() != cudaSuccess) return TCM_E_CUDA;
         if (done_launches == this_chunk && done_launches >= max_iters) {
             *deferred = true;
@@ -1432,7 +1432,7 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
         if (cudaMemcpyAsync(&act, d_active, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TCM_E_CUDA;
         if (cudaStreamSynchronize(s) != cudaSuccess) return TCM_E_CUDA;
         float ms = 0;
-        if (cudaEventElapsedTime(&ms, ev_begin, ev_end) != cudaSuccess) return TCM_E_CUDA;
+        if (ev_begin && cudaEventElapsedTime(&ms, ev_begin, ev_end) != cudaSuccess) return TCM_E_CUDA;
         *kernel_ms += ms;
         if (act == 0 || done_launches >= max_iters) break;
     }

@@ -100,15 +100,15 @@ def c4(rank=0, world=1, replicas_per_gpu=65536, n_requests=10_000, seed=4044):
     return _grid("C4", cells, seeds_total, n_requests, seed, rank_ids(len(cells), seeds_total, rank, world))
 
 
-def c4_growth(rank=0, world=1, replicas_per_gpu=4096, n_requests=2000, seed=4045):
+def c4_growth(rank=0, world=1, replicas_per_gpu=4096, n_requests=2000, seed=4045,
+              policies=(tcm.POLICY_FCFS, tcm.POLICY_TCM, tcm.POLICY_EDF)):
     """NEXT-1 memory-pressure sweep: the C4 grid (KV x lambda) under FCFS, TCM and EDF (with its
     priority-inversion preemption, R34) with decode KV growth and preemption (tcm.KV_GROWTH,
     readings R28-R32) on the stepwise engine -- the three policies of fig:preemptions
     (PAPER.md:620-623).  Footprints are clamped to kv - 2048 so that footprint + out - 1 fits the
     KV capacity (R28)."""
     base = [c for c in c4_cells() if c["policy"] == tcm.POLICY_FCFS]
-    cells = [dict(c, policy=pol, gen_kv=c["kv"] - 2048, flags=tcm.KV_GROWTH)
-             for pol in (tcm.POLICY_FCFS, tcm.POLICY_TCM, tcm.POLICY_EDF) for c in base]
+    cells = [dict(c, policy=pol, gen_kv=c["kv"] - 2048, flags=tcm.KV_GROWTH) for pol in policies for c in base]
     seeds_total = replicas_per_gpu * world // len(cells)
     return _grid("C4-growth", cells, seeds_total, n_requests, seed, rank_ids(len(cells), seeds_total, rank, world))
 

@@ -296,3 +296,38 @@ def test_c4_heavy_subset_fused_equals_stepwise_full_length():
     for k in ("iterations", "decisions", "sum_pending", "requests_done"):
         np.testing.assert_array_equal(outs[0][1][k], outs[1][1][k], err_msg=k)
     assert int(outs[0][1]["scanned_decisions"].sum()) * 10 < int(outs[0][1]["decisions"].sum())
+
+
+def test_c4_growth_fused_full_size_sampled_bit_exact():
+    # NEXT-1 at the C4 size bench.py's `next1` leg times: 65,536 replicas x 10,000 requests, FCFS and
+    # TCM cells with KV growth, fused engine (k_fgrow).  Two replicas of every cell against the
+    # full-length growth oracle, per request (admit_seq, first token, done, preempt count, preempted
+    # time); properties on all requests.
+    sw = W.c4_growth(0, 1, replicas_per_gpu=65536, n_requests=10_000,
+                     policies=(tcm.POLICY_FCFS, tcm.POLICY_TCM))
+    dev = tcm.generate_device(sw.gen)
+    dev["params"] = torch.from_numpy(sw.params.view(np.uint8)).cuda()
+    res = tcm.alloc_results(sw.n_requests, preemption=True)
+    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_FUSED, n_cells=sw.n_cells))
+    sim.load(dev, res)
+    sim.run()
+    st = sim.stats()
+    assert st["requests_done"] == sw.n_requests and st["first_bad_replica"] == -1 and st["preemptions"] > 0
+    cells = sw.params["cell_id"]
+    idx = [int(i) for c in range(sw.n_cells) for i in np.nonzero(cells == c)[0][[5, 1000]]]
+    jobs = [(sw.gen[i], int(sw.params[i]["policy"]), int(sw.params[i]["kv_capacity"]),
+             float(sw.params[i]["aging_alpha"]), int(sw.params[i]["chunk_budget"])) for i in idx]
+    with mp.get_context("spawn").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+        orc = pool.map(_oracle_growth_job, jobs, chunksize=1)
+    off = np.zeros(sw.n_replicas + 1, np.int64)
+    np.cumsum(sw.gen["n_requests"].astype(np.int64), out=off[1:])
+    for i, (s_, seq, ft, dn, pc, pt) in zip(idx, orc):
+        assert s_ == 0
+        a, b = int(off[i]), int(off[i + 1])
+        for k, v in (("admit_seq", seq), ("first_token_us", ft), ("done_us", dn), ("preempt_count", pc),
+                     ("preempted_us", pt)):
+            np.testing.assert_array_equal(res[k][a:b].cpu().numpy(), v, err_msg=f"replica {i} {k}")
+    # every request admitted once, first token before done, preempted time within its E2E
+    assert bool((res["done_us"].view(torch.int64) >= res["first_token_us"].view(torch.int64)).all())
+    assert int(res["preempt_count"].view(torch.int32).to(torch.int64).sum()) == st["preemptions"]
+    sim.close()

@@ -85,14 +85,17 @@ def check(tr, params, out, replicas):
     return dict(preemptions=tot_pre, forced=tot_forced, decisions=dec, sum_pending=sp, iterations=it)
 
 
+@pytest.mark.parametrize("engine", [tcm.ENGINE_STEPWISE, tcm.ENGINE_FUSED], ids=["stepwise", "fused"])
 @pytest.mark.parametrize("case", GOLD["cases"], ids=[c["name"] for c in GOLD["cases"]])
-def test_hand_worked_preemption_gpu(case):
+def test_hand_worked_preemption_gpu(case, engine):
+    if engine == tcm.ENGINE_FUSED and case["policy"] == "EDF":
+        pytest.skip("EDF runs on the stepwise engine only (not class-monotone)")
     tr = T.from_requests(case["requests"])
     params = tcm.make_params(1, kv_capacity=case["kv"])
     params["policy"] = {"FCFS": tcm.POLICY_FCFS, "TCM": tcm.POLICY_TCM, "EDF": tcm.POLICY_EDF}[case["policy"]]
     params["chunk_budget"] = case.get("B", 2048)
     params["flags"] = tcm.KV_GROWTH
-    out, st = run_gpu(tr, params)
+    out, st = run_gpu(tr, params, engine=engine)
     e = case["expect"]
     assert out["first_token_us"].tolist() == e["first"]
     assert out["done_us"].tolist() == e["done"]
@@ -133,7 +136,8 @@ def test_warp_per_replica_path_sampled():
 
 def test_growth_rejections():
     tr, params = growth_sweep(4, 100, 74)
-    with pytest.raises(tcm.TcmError) as e:          # the fused engine relies on Lemmas L3-L5 (R7)
+    params["policy"] = tcm.POLICY_EDF
+    with pytest.raises(tcm.TcmError) as e:          # EDF keys are not class-monotone: stepwise only
         run_gpu(tr, params, engine=tcm.ENGINE_FUSED)
     assert e.value.code == -1
     tr = T.from_requests([[0, 400, 0, 102, 0]])      # R28: 400 + 102 - 1 > 500
@@ -218,3 +222,34 @@ def test_edf_inversion_preemption_bit_exact(launch, monkeypatch):
     c = check(tr, params, out, range(48))
     assert c["preemptions"] > 0 and st["preemptions"] == c["preemptions"]
     assert st["decisions"] == c["decisions"] and st["sum_pending"] == c["sum_pending"]
+
+
+@pytest.mark.parametrize("step", [None, 5])
+def test_fused_growth_random_replicas_bit_exact(step):
+    # NEXT-1 on the fused engine (k_fgrow: class-FIFO merge + preempted stacks, R28-R32) vs the oracle
+    tr, params = growth_sweep(96, 500, 81)
+    out, st = run_gpu(tr, params, engine=tcm.ENGINE_FUSED, step=step)
+    assert st["requests_done"] == tr.n_requests and st["first_bad_replica"] == -1
+    c = check(tr, params, out, range(96))
+    assert c["preemptions"] > 0
+    assert st["preemptions"] == c["preemptions"] and st["forced_preemptions"] == c["forced"]
+    assert st["decisions"] == c["decisions"] and st["sum_pending"] == c["sum_pending"]
+    assert st["iterations"] == c["iterations"]
+
+
+def test_fused_growth_mixed_with_plain_replicas():
+    # k_fused runs the R7 replicas, k_fgrow the growth ones, in one load
+    tr, params = growth_sweep(64, 400, 82)
+    params["flags"][::2] = 0
+    out, st = run_gpu(tr, params, engine=tcm.ENGINE_FUSED)
+    c = check(tr, params, out, range(64))
+    assert st["preemptions"] == c["preemptions"]
+
+
+def test_fused_growth_tight_kv_many_preemptions():
+    # heavy memory pressure: small KV, long outputs, both policies and the alpha grid
+    tr, params = growth_sweep(64, 300, 83, kvs=(4096, 6144), rates=(4.0, 8.0))
+    out, st = run_gpu(tr, params, engine=tcm.ENGINE_FUSED)
+    c = check(tr, params, out, range(64))
+    assert c["preemptions"] > 200 and st["preemptions"] == c["preemptions"]
+    assert st["forced_preemptions"] == c["forced"]

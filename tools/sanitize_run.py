@@ -1,5 +1,5 @@
 """Small runs of every libtcm kernel path for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
-usage: sanitize_run.py {fused|step1|step8|cluster|growth|edf}  (development tool; results are also checked
+usage: sanitize_run.py {fused|step1|step8|cluster|growth|edf|fgrow}  (development tool; results are also checked
 against the oracle on the first replicas so a sanitizer-clean run is also a correct one)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,7 +12,7 @@ mode = sys.argv[1]
 R, n = (8, 300) if mode != "cluster" else (1, 3000)
 if len(sys.argv) > 3:
     R, n = int(sys.argv[2]), int(sys.argv[3])
-growth = mode in ("growth", "edf")
+growth = mode in ("growth", "edf", "fgrow")
 kv = 16384
 reps = np.array([T.make_replica(7, r, n, 4.0, (0.5, 0.2, 0.3), kv - 2048 if growth else kv) for r in range(R)])
 tr = T.generate(reps)
@@ -22,7 +22,7 @@ if growth:
     params["flags"] = tcm.KV_GROWTH
 if mode in ("step1", "step8", "cluster"):
     os.environ["TCM_SW_GROUP"] = {"step1": "1", "step8": "8", "cluster": "cluster"}[mode]
-engine = tcm.ENGINE_FUSED if mode == "fused" else tcm.ENGINE_STEPWISE
+engine = tcm.ENGINE_FUSED if mode in ("fused", "fgrow") else tcm.ENGINE_STEPWISE
 dev = tcm.to_device(tr, params)
 res = tcm.alloc_results(tr.n_requests, preemption=growth)
 sim = tcm.Simulation(tcm.config(engine=engine))
