@@ -214,7 +214,11 @@ tcm_status tcm_reset(tcm_ctx* ctx);
  * number of replicas still unfinished to *active_replicas (may be NULL).  HOST results
  * are copied back before returning.  Afterwards every result of a request that has reached
  * that stage is final; admit_seq / first_token_us / done_us of a request that has not are
- * 0xFFFFFFFF / 0 / 0. */
+ * 0xFFFFFFFF / 0 / 0.  A call with max_iterations <= 64 repeated with the same value is replayed
+ * as one CUDA graph (its launches and the active-count copy, captured on the second such call on
+ * an internal stream and launched into the context's stream; a new tcm_load_trace discards it):
+ * one host round trip per call ("minimal overhead"); tcm_stats_host.engine_ms then
+ * counts the whole graph.  The environment knob TCM_GRAPHS=0 keeps every call eager. */
 tcm_status tcm_step(tcm_ctx* ctx, uint32_t max_iterations, uint32_t* active_replicas);
 
 /* Runs every replica to completion (every request done).  TCM_E_REPLICA if a replica

@@ -582,7 +582,7 @@ __device__ __noinline__ uint64_t sw_edf_invert(const TraceDev& t, uint32_t r, ui
 // GR: some replica of the trace runs TCM_KV_GROWTH (NEXT-1); the plain instantiation compiles
 // the growth code out of the hot path.
 template <int G, bool GR, int CL>
-__global__ void __launch_bounds__(kThreads, TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
+__global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
                                                       int count_active, unsigned long long* ctr,
                                                       unsigned long long ctr_base) {
     constexpr int kGroups = kWarpsPerBlock / G;
