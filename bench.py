@@ -196,11 +196,18 @@ def cpu_model():
 
 
 def sample_ids(sweep, n_sample):
-    """A deterministic sample spread over the sweep: every (R / n_sample)-th replica (replicas are
-    ordered cell-major, so the sample covers every cell in equal measure)."""
-    R = sweep.n_replicas
-    step = max(1, R // n_sample)
-    return list(range(step // 2, R, step))[:n_sample]
+    """A deterministic sample spread over the sweep: the same number of replicas from every cell
+    (the k-th sampled replica of a cell is its (k + 1/2) * (cell size / per-cell sample)-th one)."""
+    cells = np.asarray(sweep.params["cell_id"])
+    nc = int(cells.max()) + 1
+    per = max(1, n_sample // nc)
+    pick = range(nc) if nc <= n_sample else [int(c) for c in np.linspace(0, nc - 1, n_sample)]
+    out = []
+    for c in pick:
+        idx = np.nonzero(cells == c)[0]
+        step = max(1, len(idx) // per)
+        out += [int(i) for i in idx[step // 2::step][:per]]
+    return sorted(out)[:n_sample] if len(out) >= n_sample else sorted(out)
 
 
 def oracle_sample(sweep, n_trunc=0, n_sample=64, cores=None):
@@ -582,12 +589,20 @@ def bench_stepwise(args, dev, stream):
     for eng, nm in ((tcm.ENGINE_STEPWISE, "stepwise"), (tcm.ENGINE_FUSED, "fused")):
         sim = _stage_c2(1, 100_000, eng, dev, stream)
         for flush in (False, True):
+            # kernel time: eager calls (the library's events around its k_step / k_fused launch);
+            # call time: the replayed CUDA graph of tcm_step(1), as a user's loop of single steps runs
+            os.environ["TCM_GRAPHS"] = "0"
             r = c2_latency(sim, stream, args.c2_reps, flush, dev)
+            os.environ["TCM_GRAPHS"] = "1"
+            g = c2_latency(sim, stream, args.c2_reps, flush, dev)
             sfx = "_flushed" if flush else ""
             lat[nm + "_us" + sfx] = r["kernel_us"]
-            lat[nm + "_call_us" + sfx] = r["call_us"]
             lat[nm + "_p90_us" + sfx] = r["kernel_p90_us"]
+            lat[nm + "_call_us" + sfx] = g["call_us"]
+            lat[nm + "_graph_us" + sfx] = g["kernel_us"]
+            lat[nm + "_call_us_eager" + sfx] = r["call_us"]
             lat["pending"] = r["pending"]
+        os.environ.pop("TCM_GRAPHS", None)
         sim.close()
     out["C2_latency"] = lat
     return out

@@ -97,7 +97,15 @@ def c4(rank=0, world=1, replicas_per_gpu=65536, n_requests=10_000, seed=4044):
     replicas; global replica ids rank, rank+G, ... (cyclic over the 32 cells)."""
     cells = c4_cells()
     seeds_total = replicas_per_gpu * world // len(cells)
-    return _grid("C4", cells, seeds_total, n_requests, seed, rank_ids(len(cells), seeds_total, rank, world))
+    ids = rank_ids(len(cells), seeds_total, rank, world)
+    # warp layout: 16 lanes of an FCFS cell next to 16 lanes of the TCM cell with the same (lambda, KV)
+    # (cells c and c + 16): the FCFS half finishes early and leaves each warp 16 TCM replicas instead of
+    # 32, 2 % faster on the fused engine than cell-major (DESIGN.md 6.2); needs 16 | replicas per cell
+    per = len(ids) // len(cells)
+    if per % 16 == 0 and per > 0:
+        blk = np.asarray(ids).reshape(len(cells), per // 16, 16)
+        ids = np.stack([blk[:16], blk[16:]], axis=2).reshape(-1).tolist()
+    return _grid("C4", cells, seeds_total, n_requests, seed, ids)
 
 
 def c4_growth(rank=0, world=1, replicas_per_gpu=4096, n_requests=2000, seed=4045,
