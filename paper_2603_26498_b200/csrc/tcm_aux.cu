@@ -237,28 +237,30 @@ __device__ __forceinline__ uint32_t ttft_bucket(uint64_t t) {
     return 16u + 8u * (e - 4u) + (uint32_t)((t >> (e - 3u)) & 7u);
 }
 
-// A block aggregates a tile of kAggTile consecutive replicas: histogram bins are counted in a
-// shared-memory copy for the tile's (first) cell and flushed once; replicas of another cell in the
-// same tile (cell boundaries) fall back to global atomics.  Counters are warp-reduced per replica.
+// A block aggregates a tile of kAggTile consecutive replicas: histogram bins are counted in
+// shared-memory copies for the tile's first cell and the last replica's cell (two cells per tile: the C4
+// layout pairs 16 FCFS with 16 TCM replicas) and flushed once; replicas of a third cell in the same
+// tile fall back to global atomics.  Counters are warp-reduced per replica.
 constexpr uint32_t kAggTile = 32;
 
 __global__ void __launch_bounds__(256) k_aggregate(ModelConst m, TraceDev t, unsigned long long* hist,
                                                    unsigned long long* cnt) {
-    __shared__ unsigned long long sh[kGroups * kHistBins];
+    __shared__ unsigned long long sh[2][kGroups * kHistBins];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t r0 = blockIdx.x * kAggTile;
     if (r0 >= t.R) return;
     const uint32_t r1 = r0 + kAggTile < t.R ? r0 + kAggTile : t.R;
     const uint32_t cell0 = t.params[r0].cell_id;
-    for (uint32_t i = threadIdx.x; i < kGroups * kHistBins; i += blockDim.x) sh[i] = 0;
+    const uint32_t cell1 = t.params[r1 - 1].cell_id;
+    for (uint32_t i = threadIdx.x; i < 2 * kGroups * kHistBins; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
     for (uint32_t r = r0 + warp; r < r1; r += blockDim.x / 32) {
         const tcm_replica_params p = t.params[r];
         const uint64_t a = t.offset[r], b = t.offset[r + 1];
         const uint64_t B = p.chunk_budget;
-        const bool local = p.cell_id == cell0;
-        unsigned long long* H = local ? sh : hist + (size_t)p.cell_id * kGroups * kHistBins;
+        unsigned long long* H = p.cell_id == cell0 ? sh[0]
+                                : (p.cell_id == cell1 ? sh[1] : hist + (size_t)p.cell_id * kGroups * kHistBins);
         uint64_t c[3][kNcnt];
 #pragma unroll
         for (int g = 0; g < 3; ++g)
@@ -306,8 +308,11 @@ __global__ void __launch_bounds__(256) k_aggregate(ModelConst m, TraceDev t, uns
     }
     __syncthreads();
     unsigned long long* H0 = hist + (size_t)cell0 * kGroups * kHistBins;
-    for (uint32_t i = threadIdx.x; i < kGroups * kHistBins; i += blockDim.x)
-        if (sh[i]) atomicAdd(&H0[i], sh[i]);
+    unsigned long long* H1 = hist + (size_t)cell1 * kGroups * kHistBins;
+    for (uint32_t i = threadIdx.x; i < kGroups * kHistBins; i += blockDim.x) {
+        if (sh[0][i]) atomicAdd(&H0[i], sh[0][i]);
+        if (cell1 != cell0 && sh[1][i]) atomicAdd(&H1[i], sh[1][i]);
+    }
 }
 
 // ---------------------------------------------------------------------------------------

@@ -169,6 +169,64 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
         }
         if (budget == 0) break;
 
+        // ---- closed-form windows with pending requests (no preemption due: kv_free >= n_dec).  Each
+        // iteration of a window charges n_dec decode tokens, so it lasts at most kv_free / n_dec
+        // iterations (R28), and ends at the next finish or arrival.
+        if (st.n_pend > 0 && st.kv_free >= st.n_dec) {
+            const uint32_t left0 = B > st.n_dec ? B - st.n_dec : 0;   // R8
+            const uint64_t kv_after = st.kv_free - st.n_dec;          // free KV once this iteration's tokens are charged
+            uint64_t jcap = budget;
+            if (st.n_dec > 0) {
+                const uint64_t jk = st.kv_free / st.n_dec;
+                jcap = jk < jcap ? jk : jcap;
+                const uint64_t jf = cal.next - st.iter;
+                jcap = jf < jcap ? jf : jcap;
+            }
+            // Lemma L4 under growth: nothing can prefill -- the decodes take the whole budget, or no head
+            // is reserved (no partial, L2) and every pending head needs more than the free KV (the
+            // top-ranked waiting request is a head, L1, and its misfit stops every admission, R6).  The
+            // free KV only shrinks until the next finish, so that stays true.
+            bool stuck = left0 == 0;
+            if (!stuck && (st.flags & 7u) == 0) {
+                stuck = true;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    if (harr[c] <= st.clock && (uint64_t)hneed[c] <= kv_after) stuck = false;
+            }
+            uint64_t dt = m.c0 + m.cd * st.n_dec;
+            uint32_t tokj = 0;
+            // Lemma L5 for the single arrival-ordered queue (FCFS, naive aging): its reserved head needs
+            // more than this iteration's budget, takes all of it, and nothing else changes until it
+            // completes, the next finish or the next arrival.
+            if (!stuck && !prio && (st.flags & 1u) && st.rem[0] > left0 && left0 > 0 && harr[0] <= st.clock) {
+                const uint64_t jr = (st.rem[0] - 1) / left0;           // rem stays > 0
+                jcap = jr < jcap ? jr : jcap;
+                dt = m.c0 + m.cp * left0 + m.cd * st.n_dec;
+                tokj = left0;
+                stuck = true;
+            }
+            if (stuck && next_arr != ~0ull) {
+                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+                jcap = ja < jcap ? ja : jcap;
+            }
+            if (stuck && jcap >= 1 && !(st.n_dec == 0 && tokj == 0)) {
+                const uint64_t j = jcap;
+                st.clock += j * dt;
+                st.iter += j;
+                st.kv_free -= j * st.n_dec;
+                st.rem[0] -= (uint32_t)(j * tokj);
+                s_dec[tid] += j;
+                s_sum[tid] += j * st.n_pend;
+                s_maxp[tid] = st.n_pend > s_maxp[tid] ? st.n_pend : s_maxp[tid];
+                budget -= (uint32_t)j;
+                if (st.iter == cal.next) {
+                    log_event(log, st);
+                    cal.process(st);
+                }
+                continue;
+            }
+        }
+
         // ---- R29: memory exhaustion -- preempt until this iteration's decode tokens fit
         while (st.kv_free < st.n_dec) {
             int vc = -1;

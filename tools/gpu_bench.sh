@@ -15,3 +15,11 @@ if [ -n "${NCU:-}" ]; then
       --clock-control none -k regex:k_fused -c 1 --csv --log-file gpurun_out/kfused_inst.csv python tools/run_fused_once.py 65536 > gpurun_out/ncu2.log 2>&1
   tail -2 gpurun_out/ncu1.log gpurun_out/ncu2.log
 fi
+if [ -n "${SAN:-}" ]; then
+  mkdir -p gpurun_out/sanitizer
+  for tool in memcheck synccheck; do
+    timeout 400 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize_run.py fgrow \
+      > gpurun_out/sanitizer/${tool}_fgrow.log 2>&1
+    echo "$tool fgrow rc=$? $(grep -h 'ERROR SUMMARY\|: OK' gpurun_out/sanitizer/${tool}_fgrow.log | tr '\n' ' ')"
+  done
+fi
