@@ -92,6 +92,21 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
     const bool prio = prm.policy == TCM_POLICY_TCM;
     const uint32_t B = prm.chunk_budget;
     const ClassPack* kp = t.kpack + r;
+    // FP32 priority bounds for the TCM windows (|P~ - P| <= 1e-5), as in k_fused
+    __shared__ float s_fc[3][3][kGThreads];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        s_fc[0][c][tid] = kp->fS[c];
+        s_fc[1][c][tid] = kp->fp2[c];
+        s_fc[2][c][tid] = kp->fC2[c];
+    }
+    const uint32_t zmask = kp->zero_mask;
+    const bool use_bound = kp->filter_ok != 0;
+    auto bound = [&](int c, uint64_t w) -> float {
+        return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? s_fc[0][c][tid]
+                                                              : k1_filter_f32(s_fc[0][c][tid], s_fc[1][c][tid], s_fc[2][c][tid], w);
+    };
+    bool arm = false;     // the previous decision was blocked: try L4c
 
     // the head of class c: the top of its preempted stack, else the segment cursor.  hpos = its
     // position, harr its arrival (~0: none yet / exhausted), hneed the KV it reserves when admitted
@@ -195,26 +210,116 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
             }
             uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint32_t tokj = 0;
-            // Lemma L5 for the single arrival-ordered queue (FCFS, naive aging): its reserved head needs
-            // more than this iteration's budget, takes all of it, and nothing else changes until it
-            // completes, the next finish or the next arrival.
-            if (!stuck && !prio && (st.flags & 1u) && st.rem[0] > left0 && left0 > 0 && harr[0] <= st.clock) {
-                const uint64_t jr = (st.rem[0] - 1) / left0;           // rem stays > 0
-                jcap = jr < jcap ? jr : jcap;
-                dt = m.c0 + m.cp * left0 + m.cd * st.n_dec;
-                tokj = left0;
-                stuck = true;
-            }
-            if (stuck && next_arr != ~0ull) {
+            int tokc = 0;                                 // the class whose partial head takes the tokens
+            if (next_arr != ~0ull) {
                 const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                 jcap = ja < jcap ? ja : jcap;
+            }
+            // Lemma L4c under growth (TCM): a head that does not fit ranks, now, above every head that fits
+            // even at the start of the window's last iteration -- priorities only grow (L1) and the fitting
+            // set only shrinks as the free KV does -- so every iteration of the window is blocked (R6).  FP32
+            // bounds with a 2.5e-4 margin, halving the window up to 6 times, after a blocked decision.
+            if (!stuck && arm && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
+                arm = false;
+                uint64_t j = jcap;
+                bool zero_head = false;
+                float ptop = -1.0f;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const bool pend = harr[c] <= st.clock;
+                    zero_head |= pend && ((zmask >> c) & 1u);
+                    if (pend && !((zmask >> c) & 1u) && (uint64_t)hneed[c] > kv_after) {
+                        const float pb = bound(c, st.clock - harr[c]);
+                        ptop = pb > ptop ? pb : ptop;
+                    }
+                }
+                for (int h = 0; h < 6 && j >= 2 && !zero_head && ptop >= 0.0f; ++h, j >>= 1) {
+                    const uint64_t t_end = st.clock + (j - 1) * dt;
+                    float pfit = -1.0f;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        if (harr[c] <= st.clock && (uint64_t)hneed[c] <= kv_after) {
+                            const float pb = bound(c, t_end - harr[c]);
+                            pfit = pb > pfit ? pb : pfit;
+                        }
+                    }
+                    if (ptop - pfit > 2.5e-4f) {
+                        stuck = true;
+                        jcap = j;
+                        break;
+                    }
+                }
+            }
+            // Lemma L5 under growth: a reserved (partial) head that needs more than this iteration's budget
+            // and outranks every other head able to take tokens (partial, or waiting and fitting) takes the
+            // whole budget while nothing else changes: no admission, no first token, n_dec fixed until the
+            // next finish, the free KV only shrinking.  FCFS / naive aging: one queue, its head.  TCM: the
+            // partial's FP32 bound now exceeds every other candidate's at the window's last iteration.
+            if (!stuck && (st.flags & 7u) && left0 > 0 && (!prio || use_bound)) {
+                int top = -1;
+                float ptop = -1.0f;
+                uint32_t cand = 0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (harr[c] <= st.clock && (((st.flags >> c) & 1u) || (uint64_t)hneed[c] <= kv_after)) {
+                        cand |= 1u << c;
+                        const float pb = prio ? bound(c, st.clock - harr[c]) : 0.0f;
+                        if (top < 0 || pb > ptop) {
+                            top = c;
+                            ptop = pb;
+                        }
+                    }
+                }
+                uint32_t rt = 0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    if (c == top) rt = ((st.flags >> c) & 1u) ? st.rem[c] : 0;
+                if (rt > left0) {
+                    const uint64_t dt5 = m.c0 + m.cp * left0 + m.cd * st.n_dec;
+                    uint64_t j = (rt - 1) / left0;                     // rem stays > 0
+                    j = jcap < j ? jcap : j;                           // budget, finish, kv / n_dec
+                    if (next_arr != ~0ull) {
+                        const uint64_t ja = (next_arr - st.clock + dt5 - 1) / dt5;
+                        j = ja < j ? ja : j;
+                    }
+                    cand &= ~(1u << top);
+                    bool ok = j >= 1;
+                    if (prio && cand) {
+                        ok = false;
+                        for (int h = 0; h < 6 && j >= 1; ++h, j >>= 1) {
+                            const uint64_t t_end = st.clock + (j - 1) * dt5;
+                            float pmax = -1.0f;
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                if ((cand >> c) & 1u) {
+                                    const float pb = bound(c, t_end - harr[c]);
+                                    pmax = pb > pmax ? pb : pmax;
+                                }
+                            }
+                            if (ptop - pmax > 2.5e-4f) {
+                                ok = true;
+                                break;
+                            }
+                        }
+                    }
+                    if (ok) {
+                        stuck = true;
+                        jcap = j;
+                        dt = dt5;
+                        tokj = left0;
+                        tokc = top;
+                    }
+                }
             }
             if (stuck && jcap >= 1 && !(st.n_dec == 0 && tokj == 0)) {
                 const uint64_t j = jcap;
                 st.clock += j * dt;
                 st.iter += j;
                 st.kv_free -= j * st.n_dec;
-                st.rem[0] -= (uint32_t)(j * tokj);
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    if (c == tokc) st.rem[c] -= (uint32_t)(j * tokj);
+                if (tokj == 0) arm = true;                        // still blocked: try L4c again next
                 s_dec[tid] += j;
                 s_sum[tid] += j * st.n_pend;
                 s_maxp[tid] = st.n_pend > s_maxp[tid] ? st.n_pend : s_maxp[tid];
@@ -413,6 +518,7 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                 }
             }
         }
+        arm = tok == 0 && blocked;
         if (tok == 0 && st.n_dec == 0) {                   // unreachable under R6
             t.state[r].status = ST_DEADLOCK;
             st.flags |= FLAG_FINISHED;
