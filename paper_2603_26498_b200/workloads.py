@@ -31,6 +31,7 @@ class Sweep:
     params: np.ndarray       # tcm.PARAMS_DTYPE [R]
     n_cells: int
     cells: list              # human-readable description of each cell
+    ids: np.ndarray = None   # global replica id of each replica, in load order
 
     @property
     def n_replicas(self) -> int:
@@ -65,7 +66,7 @@ def _grid(name, cells, replicas_per_cell, n_requests, seed, replica_ids):
         params[j]["chunk_budget"] = c["budget"]
         params[j]["cell_id"] = g % nc
         params[j]["flags"] = c.get("flags", 0)
-    return Sweep(name, gen, params, nc, cells)
+    return Sweep(name, gen, params, nc, cells, np.asarray(replica_ids, dtype=np.int64))
 
 
 ALPHAS = [0.0] + [2.0 ** e for e in range(-7, 8)]          # R14: {0} U {2^-7 .. 2^7}

@@ -52,7 +52,7 @@ def _worker(rank, world, port, q):
     sw = W.c4(rank, world, replicas_per_gpu=REPLICAS // world, n_requests=REQUESTS)
     hist, cnt, out, st = run_shard(sw)
     W.allreduce_aggregate(hist, cnt)           # CUDA tensors over gloo
-    q.put((rank, hist.cpu().numpy(), cnt.cpu().numpy(), out, st["requests_done"]))
+    q.put((rank, hist.cpu().numpy(), cnt.cpu().numpy(), out, st["requests_done"], sw.ids))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -74,16 +74,16 @@ def test_two_ranks_through_libtcm_equal_one():
         assert p.exitcode == 0
     got.sort(key=lambda g: g[0])
     assert sum(g[4] for g in got) == full.n_requests
-    for rank, h, c, out, _ in got:
+    assert sorted(np.concatenate([g[5] for g in got]).tolist()) == sorted(full.ids.tolist())
+    for rank, h, c, out, _, gids in got:
         np.testing.assert_array_equal(h, H)       # all-reduced = single process, bit-exact
         np.testing.assert_array_equal(c, C)
-        # shard rank's replicas are global ids rank_ids(...): locate them in the single run
-        gids = W.rank_ids(len(full.cells), REPLICAS // len(full.cells), rank, 2)
-        pos = {g: j for j, g in enumerate(W.rank_ids(len(full.cells), REPLICAS // len(full.cells), 0, 1))}
+        # the shard's replicas by global id, located in the single run (both apply the C4 warp layout)
+        pos = {int(g): j for j, g in enumerate(full.ids)}
         off1 = np.concatenate([[0], np.cumsum(full.gen["n_requests"].astype(np.int64))])
         off = 0
         for g in gids:
-            j = pos[g]
+            j = pos[int(g)]
             a, b = int(off1[j]), int(off1[j + 1])
             for k in out:
                 np.testing.assert_array_equal(out[k][off:off + b - a], out1[k][a:b], err_msg=f"rank {rank} g {g} {k}")
