@@ -37,14 +37,15 @@ struct tcm_ctx {
     cudaEvent_t ev[7] = {};              // reset begin/end, engine begin/end, stamp end, k_step begin/end
     bool reset_pending = false;          // ev[0..1] recorded, not yet read
     double reset_ms = 0, engine_ms = 0, stamp_ms = 0;
-    // tcm_step(n <= kGraphMaxIters): the call's launches (budget / k_step or k_fused + stamp, the
+    // tcm_step(n <= kGraphMaxIters): the call's launches (k_step, or k_fused + stamp with the
     // events and the active-count copy) replayed as one CUDA graph per n, captured on the second
     // call with that n (the first one runs eagerly: it also initialises per-device launch caches)
     struct Graph { uint32_t iters; cudaGraphExec_t exec; uint64_t launches; bool deferred; };
     std::vector<Graph> graphs;
     std::vector<uint32_t> graph_seen;
     std::vector<uint32_t> graph_never;   // n whose capture failed: always eager
-    uint32_t* h_active = nullptr;        // pinned: the graphs' copy target
+    uint32_t* h_active = nullptr;        // pinned: the graphs' active-count target
+    uint32_t* h_active_dev = nullptr;    // its mapped device address (stepwise graphs: k_step writes it)
     cudaStream_t cs = nullptr;           // capture stream (the caller's may be the legacy stream,
                                          // which cannot be captured; a graph launches into any stream)
 };
@@ -222,7 +223,7 @@ tcm_status reset_state(tcm_ctx* c) {
     launch_init(t, s);
     c->launches++;
     if (c->cfg.engine == TCM_ENGINE_STEPWISE) {
-        stepwise_init(t, s);
+        stepwise_init(t, c->sw, s);
         c->launches++;
     } else {
         launch_fused_prologue(c->m, t, s);      // a1: class segments
@@ -250,10 +251,15 @@ tcm_status enqueue_engine(tcm_ctx* c, uint32_t max_iters, uint32_t* active_dst, 
         *launches += 2;
     } else {
         double kms = 0;
-        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, c->d_active, c->s, launches,
-                                     timed ? c->ev[5] : nullptr, timed ? c->ev[6] : nullptr, &kms, deferred);
+        // captured (graph) calls: the last k_step CTA writes the count straight into the mapped
+        // host word, so the graph is the k_step launch alone
+        const bool direct = !timed && active_dst == c->h_active && c->h_active_dev;
+        tcm_status st = stepwise_run(c->m, c->t, c->sw, max_iters, direct ? c->h_active_dev : c->d_active, c->s,
+                                     launches, timed ? c->ev[5] : nullptr, timed ? c->ev[6] : nullptr, &kms, deferred);
         c->engine_ms += kms;
         if (st != TCM_OK) return fail(c, st, "stepwise engine failed: %s", cudaGetErrorString(cudaGetLastError()));
+        TCM_CUDA(c, cudaGetLastError());
+        if (direct) return TCM_OK;
     }
     TCM_CUDA(c, cudaGetLastError());
     if (timed && c->cfg.engine != TCM_ENGINE_FUSED) TCM_CUDA(c, cudaEventRecord(c->ev[3], c->s));
@@ -374,6 +380,10 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
         c->h_active = nullptr;                      // no pinned word: short calls run eagerly
         cudaGetLastError();
     }
+    if (c->h_active && cudaHostGetDevicePointer((void**)&c->h_active_dev, c->h_active, 0) != cudaSuccess) {
+        c->h_active_dev = nullptr;                  // not mapped: the graph copies the count instead
+        cudaGetLastError();
+    }
     if (e != cudaSuccess) {
         fail(nullptr, TCM_E_CUDA, "tcm_create: %s", cudaGetErrorString(e));
         cudaFree(c->d_active);
@@ -482,7 +492,7 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
         if ((st = dalloc(c, &p, N ? N : 1))) return st;
         t.req_state = (uint8_t*)p;
         if ((st = dalloc(c, &p, stepwise_extra_bytes(R, N)))) return st;
-        c->sw = stepwise_bind(p, R);
+        c->sw = stepwise_bind(p, R, N);
         if ((st = dalloc(c, &p, 8 * (N ? N : 1)))) return st;
         t.deadline = (uint64_t*)p;
         // NEXT-1 (TCM_KV_GROWTH) per-request state and results
@@ -515,6 +525,7 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     TCM_CUDA(c, cudaStreamSynchronize(s));
     c->t.any_growth = t.any_growth = hv[2] & 1u;
     c->t.all_growth = t.all_growth = (hv[2] & 2u) == 0;
+    c->t.all_tcm = t.all_tcm = (hv[2] & 4u) == 0;
     if (c->cfg.engine == TCM_ENGINE_FUSED && t.any_growth && hv[0] == ST_OK) {
         // NEXT-1 on the fused engine (k_fgrow): per-position state, per-class stacks, preemption results
         const uint64_t P = N + 6ull * R;

@@ -113,7 +113,9 @@ __global__ void k_validate(TraceDev t, uint32_t* v, int general_ok) {
         }
     }
     // ST_BAD_INPUT (2) vs ST_CAPACITY (3): report the larger code
-    if (lane == 0) atomicOr(&v[2], growth ? 1u : 2u);      // bit 0: some replica grows; bit 1: some does not
+    // bit 0: some replica grows; bit 1: some does not; bit 2: some replica is not plain TCM
+    const bool plain_tcm = p.policy == TCM_POLICY_TCM && !(p.flags & TCM_ADMIT_SKIP);
+    if (lane == 0) atomicOr(&v[2], (growth ? 1u : 2u) | (plain_tcm ? 0u : 4u));
     const uint32_t worst = __reduce_max_sync(0xFFFFFFFFu, bad);
     if (lane == 0 && worst != ST_OK) {
         atomicMax(&v[0], worst);

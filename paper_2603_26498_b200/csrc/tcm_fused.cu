@@ -37,7 +37,26 @@ constexpr uint32_t kThreads = kFThreads;
 #ifndef TCM_FUSED_REUSEJ
 #define TCM_FUSED_REUSEJ 0
 #endif
+#ifndef TCM_FUSED_XARR
+#define TCM_FUSED_XARR 0
+#endif
+#ifndef TCM_FUSED_EAGER
+#define TCM_FUSED_EAGER 0
+#endif
+#ifndef TCM_FUSED_L4C2
+#define TCM_FUSED_L4C2 TCM_FUSED_EAGER
+#endif
 }  // namespace
+
+// Development instrumentation (build variant -DTCM_VAR_FSTATS=1 only): pass types and what ends
+// each closed-form window, per-thread counters in shared memory flushed once per thread; read by
+// tools/probe_fstats.py through tcm_dev_fstats.
+#ifdef TCM_VAR_FSTATS
+__device__ unsigned long long g_fstats[16];
+#define FSTAT(k, v) (s_fst[k][threadIdx.x] += (uint32_t)(v))
+#else
+#define FSTAT(k, v) ((void)0)
+#endif
 
 // ---------------------------------------------------------------------------------------
 // Prologue (row a1's classification, once per request): one warp per replica builds the three
@@ -113,6 +132,10 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     ReplicaState st = t.state[r];
     if (st.flags & FLAG_FINISHED) return;
     const uint32_t tid = threadIdx.x;
+#ifdef TCM_VAR_FSTATS
+    __shared__ uint32_t s_fst[16][kThreads];
+    for (int k = 0; k < 16; ++k) s_fst[k][tid] = 0;
+#endif
     s_dec[tid] = st.decisions;
     s_sum[tid] = st.sum_pending;
     s_ff[tid] = st.ff_iters;
@@ -201,6 +224,33 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS(c) : k1_filter_f32(fS(c), fp2(c), fC2(c), w);
     };
     bool arm = false;     // the previous decision was blocked: try Lemma L4c once
+#if TCM_FUSED_XARR
+    // Windows through arrivals (L4, L4c, L5): when every class queue is non-empty (FCFS: its one
+    // queue), an arrival joins its queue behind the head (L1) and changes neither a head nor kv_free
+    // nor n_dec, so a blocked or partial-continuation window does not end there.  It only adds to
+    // the pending count from the iteration that ingests it: k_a = ceil((a - clock) / dt).  Returns
+    // the sum of k_a over the arrivals ingested inside the window [0, j) and ingests them; the
+    // window's pending sum is then j * n_pend(after) - that sum (R17).
+    auto heads_full = [&]() -> bool {
+        return prio ? (harr[0] <= st.clock && harr[1] <= st.clock && harr[2] <= st.clock) : harr[0] <= st.clock;
+    };
+    auto absorb = [&](uint64_t j, uint64_t dt) -> uint64_t {
+        const uint64_t last = st.clock + (j - 1) * dt;     // start of the window's last iteration
+        uint64_t sk = 0;
+        while (next_arr <= last) {
+            const uint64_t x = next_arr - st.clock;        // 1 <= x <= (j - 1) dt
+            uint64_t ka = (uint64_t)ceil((double)x / (double)dt);
+            while (ka * dt < x) ++ka;                      // exact ceiling (fix-ups for rounding)
+            while ((ka - 1) * dt >= x) --ka;
+            sk += ka;
+            st.n_pend++;
+            st.nxt++;
+            next_arr = next_arr2;
+            next_arr2 = st.nxt + 1 < n ? arr[st.nxt + 1] : ~0ull;
+        }
+        return sk;
+    };
+#endif
 
     for (;;) {
         // ---- a1: arrivals <= clock join the pending set (their class queue already holds them)
@@ -211,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             next_arr2 = st.nxt + 1 < n ? arr[st.nxt + 1] : ~0ull;
         }
 
+        FSTAT(0, 1);
         if (st.n_pend == 0) {
             if (st.n_dec == 0) {
                 if (st.nxt == n) {                      // every request served
@@ -231,6 +282,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 j = ja < j ? ja : j;
             }
             j = j < budget ? j : budget;
+            FSTAT(1, 1);
+            FSTAT(6, st.iter + j == F);
+            FSTAT(11, j);
             st.clock += j * dt;
             st.iter += j;
             s_ff[tid] += j;
@@ -262,11 +316,16 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         // (R6); with no partial (flags) nothing prefills.  FP32 bounds only (rigorous, 2.5e-4
         // margin); tried after a blocked decision, halving the window up to 6 times.
         uint64_t l4c_j = ~0ull;
-        if (!stuck && arm && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
+        if (!stuck && (arm || TCM_FUSED_EAGER) && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
             arm = false;
+            FSTAT(10, 1);
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = cal.next - st.iter;
-            if (next_arr != ~0ull) {
+            if (next_arr != ~0ull
+#if TCM_FUSED_XARR
+                && !heads_full()
+#endif
+            ) {
                 const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                 j = ja < j ? ja : j;
             }
@@ -278,10 +337,42 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 const bool pend = harr[c] <= st.clock;
                 zero_head |= pend && ((zmask >> c) & 1u);
                 if (pend && !((zmask >> c) & 1u) && (uint64_t)hf[c] > st.kv_free) {
-                    const float p = k1_filter_f32(fS(c), fp2(c), fC2(c), st.clock - harr[c]);
+                    const float p = bound(c, st.clock - harr[c]);
                     ptop = p > ptop ? p : ptop;
                 }
             }
+#if TCM_FUSED_L4C2
+            // Window search, one copy of the bound code: the full window j; then j = 1 (is this
+            // decision itself provably blocked?  If not, the scan decides); then j/2, j/4, ... >= 2,
+            // the first success taken, else the one blocked iteration.  A blocked decision with no
+            // partial prefills nothing (R6): the scan's outcome without the scan.
+            uint64_t cand = j;
+            for (int step = 0; step < 7 && cand >= 1 && !zero_head && ptop >= 0.0f; ++step) {
+                const uint64_t t_end = st.clock + (cand - 1) * dt;
+                float pfit = -1.0f;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (harr[c] <= st.clock && (uint64_t)hf[c] <= st.kv_free) {
+                        const float p = bound(c, t_end - harr[c]);
+                        pfit = p > pfit ? p : pfit;
+                    }
+                }
+                const bool ok = ptop - pfit > 2.5e-4f;
+                if (step == 1) {
+                    if (!ok) break;
+                    l4c_j = 1;
+                    cand = j >> 1;
+                } else {
+                    if (ok) {
+                        l4c_j = cand;
+                        break;
+                    }
+                    cand = step == 0 ? (cand == 1 ? 0 : 1) : cand >> 1;
+                }
+                if (step >= 1 && cand < 2) break;
+            }
+            if (l4c_j != ~0ull) stuck = true;
+#else
             for (int h = 0; h < 6 && j >= 2 && !zero_head && ptop >= 0.0f; ++h, j >>= 1) {
                 const uint64_t t_end = st.clock + (j - 1) * dt;
                 float pfit = -1.0f;
@@ -298,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                     break;
                 }
             }
+#endif
         }
         if (stuck && st.n_dec > 0) {
             const uint64_t F = cal.next;
@@ -314,16 +406,42 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             }
 #else
             uint64_t j = F - st.iter;
-            if (next_arr != ~0ull) {
+#if TCM_FUSED_XARR
+            const bool xq = heads_full();
+#else
+            const bool xq = false;
+#endif
+            if (next_arr != ~0ull && !xq) {
                 const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                 j = ja < j ? ja : j;
             }
             j = j < budget ? j : budget;
             j = j < l4c_j ? j : l4c_j;
 #endif
+#ifdef TCM_VAR_FSTATS
+            {
+                FSTAT(l4c_j == ~0ull ? 2 : 3, 1);
+                FSTAT(6, st.iter + j == F);
+                FSTAT(11, j);
+                const bool at_arr = next_arr != ~0ull && st.clock + j * dt >= next_arr && st.iter + j != F;
+                FSTAT(7, at_arr);
+                FSTAT(8, at_arr && (prio ? harr[0] <= st.clock && harr[1] <= st.clock && harr[2] <= st.clock : harr[0] <= st.clock));
+                FSTAT(9, l4c_j != ~0ull && j == l4c_j && st.iter + j != F && !at_arr);
+            }
+#endif
+#if TCM_FUSED_XARR
+            if (xq && next_arr <= st.clock + (j - 1) * dt) {
+                const uint64_t sk = absorb(j, dt);
+                decided(j, st.n_pend);
+                s_sum[tid] -= sk;
+            } else {
+                decided(j, st.n_pend);
+            }
+#else
+            decided(j, st.n_pend);
+#endif
             st.clock += j * dt;
             st.iter += j;
-            decided(j, st.n_pend);
             budget -= (uint32_t)j;
             if (st.iter == F) {
                 log_event(log, st);
@@ -367,7 +485,12 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 uint64_t j = (rt - 1) / left;                   // rem stays > 0
                 const uint64_t jf = F - st.iter;
                 j = jf < j ? jf : j;
-                if (next_arr != ~0ull) {
+#if TCM_FUSED_XARR
+                const bool xq = heads_full();
+#else
+                const bool xq = false;
+#endif
+                if (next_arr != ~0ull && !xq) {
                     const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                     j = ja < j ? ja : j;
                 }
@@ -393,12 +516,25 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                     }
                 }
                 if (ok) {
+                    FSTAT(4, 1);
+                    FSTAT(6, st.iter + j == F);
+                    FSTAT(11, j);
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
                         if (c == top) st.rem[c] -= (uint32_t)(j * left);
+#if TCM_FUSED_XARR
+                    if (xq && next_arr <= st.clock + (j - 1) * dt) {
+                        const uint64_t sk = absorb(j, dt);
+                        decided(j, st.n_pend);
+                        s_sum[tid] -= sk;
+                    } else {
+                        decided(j, st.n_pend);
+                    }
+#else
+                    decided(j, st.n_pend);
+#endif
                     st.clock += j * dt;
                     st.iter += j;
-                    decided(j, st.n_pend);
                     budget -= (uint32_t)j;
                     if (st.iter == F) {
                         log_event(log, st);
@@ -554,6 +690,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             }
         }
         arm = tok == 0 && blocked;
+        FSTAT(5, 1);
+        FSTAT(12, tok == 0);
+        FSTAT(13, ncomp == 0 && inl_sum == 0 && tok > 0);
         if (tok == 0 && st.n_dec == 0) {                    // unreachable under R6
             t.state[r].status = ST_DEADLOCK;
             st.flags |= FLAG_FINISHED;
@@ -575,6 +714,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     }
 
     asm volatile("cp.async.wait_all;" ::: "memory");
+#ifdef TCM_VAR_FSTATS
+    for (int k = 0; k < 16; ++k) atomicAdd(&g_fstats[k], (unsigned long long)s_fst[k][tid]);
+#endif
     st.done_count = st.nxt - st.n_pend - st.n_dec;     // every arrived request is pending, decoding or done
 #undef fS
 #undef fp2
@@ -651,6 +793,20 @@ __global__ void k_fstamp(TraceDev t, uint32_t wpr) {
         }
     }
 }
+
+#ifdef TCM_VAR_FSTATS
+}  // namespace tcm
+extern "C" int tcm_dev_fstats(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, tcm::g_fstats, sizeof(tcm::g_fstats)) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(tcm::g_fstats, z, sizeof(z));
+    }
+    return 0;
+}
+namespace tcm {
+#endif
 
 void launch_fused_prologue(const ModelConst& m, const TraceDev& t, cudaStream_t s) {
     const uint32_t threads = 256;

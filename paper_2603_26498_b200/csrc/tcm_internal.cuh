@@ -139,6 +139,7 @@ struct TraceDev {
     uint64_t* ptime;         // [N] preempted time (result)
     uint32_t any_growth;     // some replica sets TCM_KV_GROWTH (from k_validate)
     uint32_t all_growth;     // every replica does
+    uint32_t all_tcm;        // every replica runs plain TCM (no EDF / FCFS / aging policy, no skip admission)
     FusedWs fw;              // fused engine only
     FGrowWs fg;              // fused engine with some TCM_KV_GROWTH replica only
 };

@@ -60,6 +60,15 @@ constexpr uint8_t RS_DEC = 32, RS_PREV = 64, RS_GEN = 128;
 constexpr int kStages = TCM_SW_STAGES;
 constexpr size_t kRingBytes = (size_t)kWarpsPerBlock * kStages * (128 * 8 + 32 * 4);
 
+// Development instrumentation (build variant -DTCM_VAR_SWSTATS=1 only): per-launch event counts
+// of k_step's warp-per-replica path, read by tools/probe_swstats.py through tcm_dev_swstats.
+#ifdef TCM_VAR_SWSTATS
+__device__ unsigned long long g_swstats[16];
+#define SWSTAT(k, v) do { if (lane == 0) atomicAdd(&g_swstats[k], (unsigned long long)(v)); } while (0)
+#else
+#define SWSTAT(k, v) do { } while (0)
+#endif
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
@@ -268,17 +277,20 @@ __device__ __forceinline__ void gsync() {
 
 // Prologue (warp 0 of the group): ingest, idle jumps, decode-only fast-forward.
 // mode: 0 = nothing more this launch, 1 = decision iteration.
-template <int G, bool GR>
-__device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, GroupSmem<G>& sm, int lane) {
+// budget != 0: the call's first launch sets the call's iteration budget (head[1]).
+template <int G, bool GR, bool TO>
+__device__ void sw_prologue(const ModelConst& m, const TraceDev& t, uint32_t r, GroupSmem<G>& sm, int lane,
+                            uint32_t budget) {
     ReplicaState st = t.state[r];
+    if (budget) st.head[1] = budget;
     const uint64_t base = t.offset[r];
     const uint32_t n = (uint32_t)(t.offset[r + 1] - base);
     const uint64_t* arr = t.arrival + base;
     const uint32_t* fp = t.footprint + base;
     const uint8_t* mod = t.mod + base;
     uint8_t* rs = t.req_state + base;
-    const bool prio = t.params[r].policy == TCM_POLICY_TCM;
-    const bool edf = t.params[r].policy == TCM_POLICY_EDF;
+    const bool prio = TO || t.params[r].policy == TCM_POLICY_TCM;
+    const bool edf = !TO && t.params[r].policy == TCM_POLICY_EDF;
     const bool growth = GR && (t.params[r].flags & TCM_KV_GROWTH) != 0;
     int mode = 0;
     if (!(st.flags & FLAG_FINISHED) && st.head[1] > 0) {
@@ -581,10 +593,11 @@ __device__ __noinline__ uint64_t sw_edf_invert(const TraceDev& t, uint32_t r, ui
 
 // GR: some replica of the trace runs TCM_KV_GROWTH (NEXT-1); the plain instantiation compiles
 // the growth code out of the hot path.
-template <int G, bool GR, int CL>
-__global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv, uint32_t* active,
-                                                      int count_active, unsigned long long* ctr,
-                                                      unsigned long long ctr_base) {
+// TO: every replica runs plain TCM (TraceDev.all_tcm): the FCFS / EDF / first-fit paths compile out
+// (a smaller kernel for the instruction cache).
+template <int G, bool GR, int CL, bool TO = false>
+__global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv,
+                                                                             StepCtl ctl) {
     constexpr int kGroups = kWarpsPerBlock / G;
     constexpr int kMaxDone = GroupSmem<G>::kMaxDone;
     __shared__ double s_lnR[16], s_lnT[16], s_expT[16];
@@ -602,6 +615,8 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
         if constexpr (CL > 1) return *cooperative_groups::this_cluster().map_shared_rank(&smg[0], 0);
         else return smg[group];
     }();
+    __shared__ uint32_t s_active;                     // this CTA's active replicas (counting launches)
+    if (tid == 0) s_active = 0;
     if (tid < 16) {
         s_lnR[tid] = kLnR[tid];
         s_lnT[tid] = kLnT[tid];
@@ -612,13 +627,12 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
 
     const uint32_t r0 = CL > 1 ? blockIdx.x / CL : blockIdx.x * kGroups + group;
     const uint32_t rstep = CL > 1 ? gridDim.x / CL : gridDim.x * kGroups;
-    // A warp per replica takes replicas from a global counter (dynamic balance; every warp of the
-    // launch ends with exactly one failing grab, so a launch advances the counter by R + warps and
-    // the host passes each launch its base); CTA and cluster groups use a static stride.
-    const bool kDyn = G == 1 && CL == 1 && ctr != nullptr;   // host passes nullptr when R <= warps
+    // A warp per replica takes replicas from a global counter (dynamic balance; the launch's last
+    // CTA resets it, see the end of the kernel); CTA and cluster groups use a static stride.
+    const bool kDyn = G == 1 && CL == 1 && ctl.dyn;          // host clears dyn when R <= warps
     auto grab = [&]() -> uint32_t {
         unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(ctr, 1ull) - ctr_base;
+        if (lane == 0) v = atomicAdd(&ctl.w->ctr, 1ull);
         v = __shfl_sync(0xFFFFFFFFu, v, 0);
         return v < t.R ? (uint32_t)v : t.R;
     };
@@ -635,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
         }
         const tcm_replica_params prm = t.params[r];
         const uint64_t base = t.offset[r];
-        if (wg == 0) sw_prologue<G, GR>(m, t, r, gsm, lane);
+        if (wg == 0) sw_prologue<G, GR, TO>(m, t, r, gsm, lane, kit == 0 ? ctl.budget : 0u);
         gsync<G, CL>();
         if (gsm.mode == 0) {
             if (wg == 0 && lane == 0) t.state[r] = gsm.st;
@@ -643,9 +657,9 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
             break;
         }
 
-        const bool prio = prm.policy == TCM_POLICY_TCM;
-        const bool edf = prm.policy == TCM_POLICY_EDF;
-        const bool skip = (prm.flags & TCM_ADMIT_SKIP) != 0;
+        const bool prio = TO || prm.policy == TCM_POLICY_TCM;
+        const bool edf = !TO && prm.policy == TCM_POLICY_EDF;
+        const bool skip = !TO && (prm.flags & TCM_ADMIT_SKIP) != 0;
         // the streamed 8-byte key input: arrival (TCM aging, FCFS) or the EDF deadline x den
         const uint64_t* arr = (edf ? t.deadline : t.arrival) + base;
         const uint32_t* fp = t.footprint + base;
@@ -677,7 +691,9 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
         const bool cmp_ok = prio && sm.kp.Smax[0] < 65536.0 && sm.kp.Smax[1] < 65536.0 && sm.kp.Smax[2] < 65536.0;
         const uint32_t zero_mask = sm.kp.zero_mask;
 
+        SWSTAT(0, 1);
         for (int pass = 0;; ++pass) {
+            SWSTAT(1, 1);
             const bool first_pass = pass == 0;
             const bool has_th = gsm.has_th;
             const uint64_t thk = gsm.thk;
@@ -704,6 +720,7 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
             uint32_t skipm = 0, tiem = 0;
             int64_t am0 = INT64_MAX, am1 = INT64_MAX, am2 = INT64_MAX, amx = INT64_MAX;   // amx = max_c am_c
             auto retune = [&]() {
+                SWSTAT(10, 1);
                 const double Pkk = __longlong_as_double((long long)kk);
                 const float thrf = __double2float_rd(Pkk);
                 skipm = 0;
@@ -752,7 +769,10 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
             uint8_t* qc = sm.qc[wl];
             auto take = [&](uint64_t key, uint32_t id, bool enter) {   // warp-collective
                 const uint32_t em = __ballot_sync(0xFFFFFFFFu, enter);
+                SWSTAT(7, 1);
                 if (em == 0) return;
+                SWSTAT(8, __popc(em) <= 16);
+                SWSTAT(9, __popc(em));
                 if (__popc(em) <= 16) {
                     // up to 16 entrants: insert each into the sorted list (rank by ballot, shift by shuffle)
                     uint32_t rest = em;
@@ -834,7 +854,13 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
                     live = !lean_path || (first_pass && (cc & RS_RES)) ||
                            (((tiem >> qcl) & 1u) ? id < ki : (int64_t)(clock - qwl) <= am);
                 }
+                SWSTAT(5, 1);
                 if (!__any_sync(0xFFFFFFFFu, live)) return;
+                SWSTAT(4, 1);
+#ifdef TCM_VAR_SWSTATS
+                const uint32_t nlive = __popc(__ballot_sync(0xFFFFFFFFu, live));
+                SWSTAT(6, nlive);
+#endif
                 if (live) {
                     const int c = cc & RS_CLS;
 #if TCM_SW_SAT
@@ -898,6 +924,7 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
                 const uint32_t s4 = rst[slot * 32 + lane];
                 const int e0 = (int)(g0 + 4 * lane);
                 bool take_chunk = true;
+                SWSTAT(2, 1);
                 if (lean) {
                     // fast rejection: arrivals after every class's limit, and no partial to record
                     // (arrivals are sorted, so a lane's first element is its smallest)
@@ -905,6 +932,7 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
                     take_chunk = __any_sync(0xFFFFFFFFu, maybe);
                 }
                 if (take_chunk) {
+                SWSTAT(3, 1);
                 uint32_t qbits = 0;                       // bit j: element j goes to the refine queue
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -1002,6 +1030,7 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
                 }
                 bool valid = li != NIL;
                 const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
+                SWSTAT(12, nvalid);
                 const uint64_t left = gsm.left;
                 const bool blocked_prev = gsm.blocked;
                 if (GR && growth && edf && !skip) {           // NEXT-3 EDF priority inversion (R34)
@@ -1162,6 +1191,7 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
             const uint64_t now = st.clock;
             const uint64_t it = st.iter;
             const int nd = gsm.ndone;
+            SWSTAT(11, nd);
             const uint16_t* out = t.out + base;
             uint32_t* cal = t.cal + (size_t)r * kCalSlots;
             uint32_t* occ = t.occ + (size_t)r * kCalWords;
@@ -1244,27 +1274,40 @@ __global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(Mod
         }
         gsync<G, CL>();
       }
-        if (wg == 0 && lane == 0 && count_active && !(gsm.st.flags & FLAG_FINISHED)) atomicAdd(active, 1u);
+        if (wg == 0 && lane == 0 && ctl.count_active && !(gsm.st.flags & FLAG_FINISHED)) atomicAdd(&s_active, 1u);
         gsync<G, CL>();
     }
     if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
+    // The launch's last CTA publishes the active-replica count to ctl.active_out (device memory,
+    // or the caller's mapped host word under graph replay) and resets the control words for the
+    // next launch on the stream: a call is then its k_step launches alone (no budget kernel, no
+    // memset, no copy node).
+    __syncthreads();
+    if (tid == 0) {
+        if (s_active) atomicAdd(&ctl.w->acc, s_active);
+        __threadfence();
+        if (atomicAdd(&ctl.w->done_ctas, 1u) == gridDim.x - 1) {
+            __threadfence();
+            const uint32_t a = atomicExch(&ctl.w->acc, 0u);
+            if (ctl.count_active) *ctl.active_out = a;
+            atomicExch(&ctl.w->ctr, 0ull);
+            atomicExch(&ctl.w->done_ctas, 0u);
+        }
+    }
 }
 
 // ReplicaState.head[0] = window start lo (oldest possibly-pending id), head[1] = remaining
 // iteration budget of the current tcm_step call; the class-queue fields are unused here.
 // Per-call iteration budget of every replica; also zeroes the active-replica count and the
 // replica counter of the dynamic mode (one launch instead of a launch and two memsets).
-__global__ void k_sw_budget(TraceDev t, uint32_t budget, uint32_t* d_active, unsigned long long* ctr) {
+// (k_step's first launch of a call sets head[1] itself: StepCtl.budget.)
+__global__ void k_sw_init(TraceDev t, StepSync* w) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < t.R) t.state[r].head[1] = budget;
     if (r == 0) {
-        *d_active = 0;
-        if (ctr) *ctr = 0;
+        w->ctr = 0;
+        w->done_ctas = 0;
+        w->acc = 0;
     }
-}
-
-__global__ void k_sw_init(TraceDev t) {
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < t.R) {
         t.state[r].head[0] = 0;
         t.state[r].head[1] = 0;
@@ -1274,18 +1317,22 @@ __global__ void k_sw_init(TraceDev t) {
     }
 }
 
-void stepwise_init(const TraceDev& t, cudaStream_t s) { k_sw_init<<<(t.R + 255) / 256, 256, 0, s>>>(t); }
+void stepwise_init(const TraceDev& t, const StepwiseWorkspace& w, cudaStream_t s) {
+    k_sw_init<<<(t.R + 255) / 256, 256, 0, s>>>(t, w.sync);
+}
 
+// rem[N], then the 16-byte StepSync (8-byte aligned)
 size_t stepwise_extra_bytes(uint32_t R, uint64_t N) {
     (void)R;
-    return 4 * N + 16;
+    return ((4 * N + 7) & ~7ull) + sizeof(StepSync);
 }
 size_t stepwise_workspace_bytes(uint32_t R, uint64_t N) { return N + stepwise_extra_bytes(R, N); }
 
-StepwiseWorkspace stepwise_bind(void* p, uint32_t R) {
+StepwiseWorkspace stepwise_bind(void* p, uint32_t R, uint64_t N) {
     StepwiseWorkspace w;
     w.base = p;
     w.R = R;
+    w.sync = reinterpret_cast<StepSync*>(reinterpret_cast<char*>(p) + ((4 * N + 7) & ~7ull));
     return w;
 }
 
@@ -1313,6 +1360,7 @@ DevFacts dev_facts() {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_step<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+        cudaFuncSetAttribute(k_step<1, false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
         cudaFuncSetAttribute(k_step<8, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
         cudaFuncSetAttribute(k_step<1, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
         cudaFuncSetAttribute(k_step<8, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
@@ -1326,6 +1374,15 @@ DevFacts dev_facts() {
         f.sms = sms;
     }
     return f;
+}
+
+// The TCM-only instantiation (TraceDev.all_tcm); TCM_SW_TO=0 forces the general one (development A/B).
+bool use_to() {
+    static const bool on = [] {
+        const char* e = getenv("TCM_SW_TO");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 Launch stepwise_config(uint32_t R, uint64_t N) {
@@ -1366,34 +1423,45 @@ Launch stepwise_config(uint32_t R, uint64_t N) {
 }
 }  // namespace
 
+#ifdef TCM_VAR_SWSTATS
+}  // namespace tcm
+extern "C" int tcm_dev_swstats(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, tcm::g_swstats, sizeof(tcm::g_swstats)) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(tcm::g_swstats, z, sizeof(z));
+    }
+    return 0;
+}
+namespace tcm {
+#endif
+
 tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWorkspace& w, uint32_t max_iters,
-                        uint32_t* d_active, cudaStream_t s, uint64_t* launches, cudaEvent_t ev_begin,
+                        uint32_t* active_out, cudaStream_t s, uint64_t* launches, cudaEvent_t ev_begin,
                         cudaEvent_t ev_end, double* kernel_ms, bool* deferred) {
     uint32_t* remv = reinterpret_cast<uint32_t*>(w.base);
-    // replica counter for the warp-per-replica mode: in the workspace's 16 spare bytes after rem
-    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(
-        reinterpret_cast<char*>(w.base) + ((4 * t.N + 7) & ~7ull));
     const Launch L = stepwise_config(t.R, t.N);
-    const unsigned long long per_launch = (unsigned long long)t.R + (unsigned long long)L.grid * kWarpsPerBlock;
-    if (L.group != 1 || L.cluster != 1 || t.R <= (uint64_t)L.grid * kWarpsPerBlock) ctr = nullptr;   // static is ideal
-    unsigned long long ctr_base = 0;
-    k_sw_budget<<<(t.R + 255) / 256, 256, 0, s>>>(t, max_iters, d_active, ctr);
-    (*launches)++;
-    // Each k_step launch advances every active replica by one iteration (or one fast-forward);
-    // launch in chunks and read the active count only at the end of each chunk.  A call that fits
-    // in one chunk (tcm_step(n <= 64)) returns without synchronising: the caller reads d_active and
-    // the events after its own (single) synchronisation (*deferred = true).
+    StepCtl ctl{};
+    ctl.w = w.sync;
+    ctl.dyn = L.group == 1 && L.cluster == 1 && t.R > (uint64_t)L.grid * kWarpsPerBlock;   // else static is ideal
+    // Each k_step launch advances every active replica by up to kItersPerLaunch iterations (tcm_step's
+    // budget, set by the call's first launch, bounds the total); launch in chunks and read the active
+    // count only at the end of each chunk.  A call that fits in one chunk (tcm_step(n <= 64)) returns
+    // without synchronising: the caller reads *active_out and the events after its own (single)
+    // synchronisation (*deferred = true).
     const uint32_t chunk = 64;
     uint64_t done_launches = 0;
     *deferred = false;
     for (;;) {
         uint32_t this_chunk = chunk;
         if ((uint64_t)max_iters - done_launches < this_chunk) this_chunk = (uint32_t)(max_iters - done_launches);
-        if (done_launches > 0 && cudaMemsetAsync(d_active, 0, 4, s) != cudaSuccess) return TCM_E_CUDA;
         // device time of the k_step launches alone (tcm_stats_host.engine_ms)
         if (ev_begin && cudaEventRecord(ev_begin, s) != cudaSuccess) return TCM_E_CUDA;   // null: untimed (graph capture)
         for (uint32_t q = 0; q < this_chunk; ++q) {
-            const int last = q + 1 == this_chunk;
+            ctl.count_active = q + 1 == this_chunk;
+            ctl.active_out = active_out;
+            ctl.budget = done_launches == 0 && q == 0 ? max_iters : 0u;
             if (L.cluster > 1) {
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(L.grid);
@@ -1408,18 +1476,19 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
                 cudaError_t e = t.any_growth
-                    ? cudaLaunchKernelEx(&cfg, k_step<8, true, kCluster>, m, t, remv, d_active, last, ctr, ctr_base)
-                    : cudaLaunchKernelEx(&cfg, k_step<8, false, kCluster>, m, t, remv, d_active, last, ctr, ctr_base);
+                    ? cudaLaunchKernelEx(&cfg, k_step<8, true, kCluster>, m, t, remv, ctl)
+                    : cudaLaunchKernelEx(&cfg, k_step<8, false, kCluster>, m, t, remv, ctl);
                 if (e != cudaSuccess) return TCM_E_CUDA;
             } else if (t.any_growth) {
-                if (L.group == 1) k_step<1, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
-                else k_step<8, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
+                if (L.group == 1) k_step<1, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, ctl);
+                else k_step<8, true, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, ctl);
             } else {
-                if (L.group == 1) k_step<1, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
-                else k_step<8, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, d_active, last, ctr, ctr_base);
+                if (L.group == 1 && t.all_tcm && use_to())
+                    k_step<1, false, 1, true><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, ctl);
+                else if (L.group == 1) k_step<1, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, ctl);
+                else k_step<8, false, 1><<<L.grid, kThreads, kRingBytes, s>>>(m, t, remv, ctl);
             }
             (*launches)++;
-            ctr_base += per_launch;
         }
         done_launches += this_chunk;
         if (ev_end && cudaEventRecord(ev_end, s) != cudaSuccess) return TCM_E_CUDA;
@@ -1429,7 +1498,7 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
             break;
         }
         uint32_t act = 0;
-        if (cudaMemcpyAsync(&act, d_active, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TCM_E_CUDA;
+        if (cudaMemcpyAsync(&act, active_out, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TCM_E_CUDA;
         if (cudaStreamSynchronize(s) != cudaSuccess) return TCM_E_CUDA;
         float ms = 0;
         if (ev_begin && cudaEventElapsedTime(&ms, ev_begin, ev_end) != cudaSuccess) return TCM_E_CUDA;

@@ -36,9 +36,12 @@ for rep in range(3):
 st = sim.stats()
 h = hashlib.sha256()
 for k in ("admit_seq", "first_token_us", "done_us"):
-    h.update(res[k].view(torch.uint8).cpu().numpy().tobytes()) if res[k].numel() < 0 else None
     x = res[k]
-    h.update(str(int(x.view(torch.int64 if x.element_size() == 8 else torch.int32).to(torch.int64).sum())).encode())
+    x = x.view(torch.int64 if x.element_size() == 8 else torch.int32).to(torch.int64)
+    w = (torch.arange(x.numel(), device=x.device, dtype=torch.int64) % 65521) + 1
+    h.update(str(int(x.sum())).encode() + b"/" + str(int((x * w).sum())).encode())
+for k in ("iterations", "decisions", "sum_pending", "requests_done"):
+    h.update(str(st[k]).encode())
 name = os.path.basename(os.environ.get("TCM_LIB_PATH", "libtcm.so"))
 print(f"{name} [{order}]: run ms {['%.1f' % t for t in ts]} engine_ms {st.get('engine_ms', 0):.1f} scanned {st['scanned_decisions']} "
       f"decisions {st['decisions']} digest {h.hexdigest()[:16]}", flush=True)
