@@ -218,7 +218,10 @@ tcm_status tcm_reset(tcm_ctx* ctx);
  * as one CUDA graph (its launches and the active-count copy, captured on the second such call on
  * an internal stream and launched into the context's stream; a new tcm_load_trace discards it):
  * one host round trip per call ("minimal overhead"); tcm_stats_host.engine_ms then
- * counts the whole graph.  The environment knob TCM_GRAPHS=0 keeps every call eager. */
+ * counts the whole graph.  STEPWISE: the graph holds only the k_step launches -- the first one
+ * sets the call's iteration budget and the launch's last CTA writes the active count into a
+ * mapped host word, so there is no budget kernel, memset or copy node.  The environment knob
+ * TCM_GRAPHS=0 keeps every call eager. */
 tcm_status tcm_step(tcm_ctx* ctx, uint32_t max_iterations, uint32_t* active_replicas);
 
 /* Runs every replica to completion (every request done).  TCM_E_REPLICA if a replica

@@ -36,8 +36,17 @@ __device__ __forceinline__ void ld_arrfp(const FRec* p, uint64_t& arr, uint32_t&
 // that makes the copy wait for a register (the value just read from the same shared slot).
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t dep) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+#ifndef TCM_FUSED_CA
+#define TCM_FUSED_CA 0
+#endif
+#if TCM_FUSED_CA
+    // .ca: the record's sector also lands in L1, where ld_inl_id_out finds id / out later
+    asm volatile("{\n\t.reg .b64 d;\n\tmov.b64 d, %2;\n\tcp.async.ca.shared.global [%0], [%1], 16;\n\t"
+                 "cp.async.commit_group;\n\t}" ::"r"(sa), "l"(gmem), "l"(dep) : "memory");
+#else
     asm volatile("{\n\t.reg .b64 d;\n\tmov.b64 d, %2;\n\tcp.async.cg.shared.global [%0], [%1], 16;\n\t"
                  "cp.async.commit_group;\n\t}" ::"r"(sa), "l"(gmem), "l"(dep) : "memory");
+#endif
 }
 // Wait until at most `newer` of this thread's most recent copy groups are still in flight.
 __device__ __forceinline__ void cp_async_wait(uint32_t newer) {

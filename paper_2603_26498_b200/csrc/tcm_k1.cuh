@@ -197,7 +197,7 @@ __device__ __forceinline__ double k1_exp_bf(double y, const K1Tables& tb) {
 // ---- FP32 bound on the priority (filter for the exact top-k; never decides an order) --------
 // P~ = S + (1 - 2^(-x log2 e)), x = 2^(p2 * log2(w) + C2), C2 = C / ln 2, evaluated with the
 // SFU approximations (PTX lg2.approx / ex2.approx, max errors 2^-22.6 abs / 2^-22.5 rel) and
-// log2(w) from the exact exponent plus the top 24 mantissa bits.  Error budget:
+// log2(w) of w rounded to FP32 (relative error <= 2^-24).  Error budget:
 // |P~ - P| <= 0.37 * ln2 * (p * 2.5e-6 + (|y| + |C2|) * 6e-8) + 1e-6, i.e. < 1e-5 for the
 // supported range (p <= 16, |C2| <= 1000); the kernel uses kFilterDelta = 1e-4, and
 // tcm_k1_filter_error() audits the bound exhaustively per (class, alpha) on the device.
@@ -215,12 +215,9 @@ __device__ __forceinline__ float sfu_ex2(float x) {
 }
 
 __device__ __forceinline__ float k1_filter_f32(float Sf, float p2, float C2, uint64_t w) {
-    const int lz = __clzll((long long)w);                 // w >= 1
-    const int e = 63 - lz;
-    const uint32_t mant = (uint32_t)((w << lz) >> 40) & 0x7FFFFFu;
-    const float M = __uint_as_float(0x3F800000u | mant);
-    const float ef = __int_as_float(0x4B000000 + e) - 8388608.0f;   // exact small int -> float
-    const float L = ef + sfu_lg2(M);
+    // w >= 1: one conversion (round to nearest, relative error <= 2^-24, half the truncation error of
+    // the exponent + top-23-mantissa-bits form it replaces) and the SFU lg2 of the float
+    const float L = sfu_lg2(__ull2float_rn(w));
     const float x = sfu_ex2(fmaf(p2, L, C2));
     const float ee = sfu_ex2(-x * 1.44269504f);
     return Sf + (1.0f - ee);
