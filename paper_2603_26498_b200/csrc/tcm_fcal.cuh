@@ -37,7 +37,7 @@ __device__ __forceinline__ void ld_arrfp(const FRec* p, uint64_t& arr, uint32_t&
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t dep) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
 #ifndef TCM_FUSED_CA
-#define TCM_FUSED_CA 0
+#define TCM_FUSED_CA 1
 #endif
 #if TCM_FUSED_CA
     // .ca: the record's sector also lands in L1, where ld_inl_id_out finds id / out later

@@ -34,18 +34,6 @@ namespace tcm {
 namespace {
 
 constexpr uint32_t kThreads = kFThreads;
-#ifndef TCM_FUSED_REUSEJ
-#define TCM_FUSED_REUSEJ 0
-#endif
-#ifndef TCM_FUSED_XARR
-#define TCM_FUSED_XARR 0
-#endif
-#ifndef TCM_FUSED_EAGER
-#define TCM_FUSED_EAGER 0
-#endif
-#ifndef TCM_FUSED_L4C2
-#define TCM_FUSED_L4C2 TCM_FUSED_EAGER
-#endif
 }  // namespace
 
 // Development instrumentation (build variant -DTCM_VAR_FSTATS=1 only): pass types and what ends
@@ -223,34 +211,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     auto bound_dyn = [&](int c, uint64_t w) -> float {     // c not known at compile time
         return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS(c) : k1_filter_f32(fS(c), fp2(c), fC2(c), w);
     };
-    bool arm = false;     // the previous decision was blocked: try Lemma L4c once
-#if TCM_FUSED_XARR
-    // Windows through arrivals (L4, L4c, L5): when every class queue is non-empty (FCFS: its one
-    // queue), an arrival joins its queue behind the head (L1) and changes neither a head nor kv_free
-    // nor n_dec, so a blocked or partial-continuation window does not end there.  It only adds to
-    // the pending count from the iteration that ingests it: k_a = ceil((a - clock) / dt).  Returns
-    // the sum of k_a over the arrivals ingested inside the window [0, j) and ingests them; the
-    // window's pending sum is then j * n_pend(after) - that sum (R17).
-    auto heads_full = [&]() -> bool {
-        return prio ? (harr[0] <= st.clock && harr[1] <= st.clock && harr[2] <= st.clock) : harr[0] <= st.clock;
-    };
-    auto absorb = [&](uint64_t j, uint64_t dt) -> uint64_t {
-        const uint64_t last = st.clock + (j - 1) * dt;     // start of the window's last iteration
-        uint64_t sk = 0;
-        while (next_arr <= last) {
-            const uint64_t x = next_arr - st.clock;        // 1 <= x <= (j - 1) dt
-            uint64_t ka = (uint64_t)ceil((double)x / (double)dt);
-            while (ka * dt < x) ++ka;                      // exact ceiling (fix-ups for rounding)
-            while ((ka - 1) * dt >= x) --ka;
-            sk += ka;
-            st.n_pend++;
-            st.nxt++;
-            next_arr = next_arr2;
-            next_arr2 = st.nxt + 1 < n ? arr[st.nxt + 1] : ~0ull;
-        }
-        return sk;
-    };
-#endif
 
     for (;;) {
         // ---- a1: arrivals <= clock join the pending set (their class queue already holds them)
@@ -314,18 +274,14 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         // start of the window's last iteration.  Priorities only grow with waiting time (L1), so
         // at every iteration of the window the top-ranked head misfits and blocks all admissions
         // (R6); with no partial (flags) nothing prefills.  FP32 bounds only (rigorous, 2.5e-4
-        // margin); tried after a blocked decision, halving the window up to 6 times.
+        // margin).  Tried before every decision with a misfitting head and no partial: a window of
+        // one iteration is this decision itself, blocked, decided without the scan.
         uint64_t l4c_j = ~0ull;
-        if (!stuck && (arm || TCM_FUSED_EAGER) && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
-            arm = false;
+        if (!stuck && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
             FSTAT(10, 1);
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = cal.next - st.iter;
-            if (next_arr != ~0ull
-#if TCM_FUSED_XARR
-                && !heads_full()
-#endif
-            ) {
+            if (next_arr != ~0ull) {
                 const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                 j = ja < j ? ja : j;
             }
@@ -341,7 +297,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                     ptop = p > ptop ? p : ptop;
                 }
             }
-#if TCM_FUSED_L4C2
             // Window search, one copy of the bound code: the full window j; then j = 1 (is this
             // decision itself provably blocked?  If not, the scan decides); then j/2, j/4, ... >= 2,
             // the first success taken, else the one blocked iteration.  A blocked decision with no
@@ -372,52 +327,17 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 if (step >= 1 && cand < 2) break;
             }
             if (l4c_j != ~0ull) stuck = true;
-#else
-            for (int h = 0; h < 6 && j >= 2 && !zero_head && ptop >= 0.0f; ++h, j >>= 1) {
-                const uint64_t t_end = st.clock + (j - 1) * dt;
-                float pfit = -1.0f;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    if (harr[c] <= st.clock && (uint64_t)hf[c] <= st.kv_free) {
-                        const float p = k1_filter_f32(fS(c), fp2(c), fC2(c), t_end - harr[c]);
-                        pfit = p > pfit ? p : pfit;
-                    }
-                }
-                if (ptop - pfit > 2.5e-4f) {
-                    stuck = true;
-                    l4c_j = j;
-                    break;
-                }
-            }
-#endif
         }
         if (stuck && st.n_dec > 0) {
             const uint64_t F = cal.next;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
-#if TCM_FUSED_REUSEJ
-            uint64_t j = l4c_j;              // L4c's window is within the event / arrival / budget caps already
-            if (l4c_j == ~0ull) {
-                j = F - st.iter;
-                if (next_arr != ~0ull) {
-                    const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
-                    j = ja < j ? ja : j;
-                }
-                j = j < budget ? j : budget;
-            }
-#else
             uint64_t j = F - st.iter;
-#if TCM_FUSED_XARR
-            const bool xq = heads_full();
-#else
-            const bool xq = false;
-#endif
-            if (next_arr != ~0ull && !xq) {
+            if (next_arr != ~0ull) {
                 const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                 j = ja < j ? ja : j;
             }
             j = j < budget ? j : budget;
             j = j < l4c_j ? j : l4c_j;
-#endif
 #ifdef TCM_VAR_FSTATS
             {
                 FSTAT(l4c_j == ~0ull ? 2 : 3, 1);
@@ -429,17 +349,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 FSTAT(9, l4c_j != ~0ull && j == l4c_j && st.iter + j != F && !at_arr);
             }
 #endif
-#if TCM_FUSED_XARR
-            if (xq && next_arr <= st.clock + (j - 1) * dt) {
-                const uint64_t sk = absorb(j, dt);
-                decided(j, st.n_pend);
-                s_sum[tid] -= sk;
-            } else {
-                decided(j, st.n_pend);
-            }
-#else
             decided(j, st.n_pend);
-#endif
             st.clock += j * dt;
             st.iter += j;
             budget -= (uint32_t)j;
@@ -447,10 +357,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 log_event(log, st);
                 cal.process(st);
             }
-            arm = true;                                     // still blocked: try L4c again next
             continue;
         }
-        arm = false;
 
         // ---- Lemma L5: a partial prefill that outranks every other head able to take tokens
         // (partial, or waiting and fitting the free KV) and needs more than this iteration's
@@ -485,12 +393,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 uint64_t j = (rt - 1) / left;                   // rem stays > 0
                 const uint64_t jf = F - st.iter;
                 j = jf < j ? jf : j;
-#if TCM_FUSED_XARR
-                const bool xq = heads_full();
-#else
-                const bool xq = false;
-#endif
-                if (next_arr != ~0ull && !xq) {
+                if (next_arr != ~0ull) {
                     const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
                     j = ja < j ? ja : j;
                 }
@@ -522,17 +425,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
                         if (c == top) st.rem[c] -= (uint32_t)(j * left);
-#if TCM_FUSED_XARR
-                    if (xq && next_arr <= st.clock + (j - 1) * dt) {
-                        const uint64_t sk = absorb(j, dt);
-                        decided(j, st.n_pend);
-                        s_sum[tid] -= sk;
-                    } else {
-                        decided(j, st.n_pend);
-                    }
-#else
                     decided(j, st.n_pend);
-#endif
                     st.clock += j * dt;
                     st.iter += j;
                     budget -= (uint32_t)j;
@@ -566,17 +459,15 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             pf[c] = (prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
         }
         while (left > 0) {
+            // tournament over the eligible heads carrying only the leader's index (its bound, key,
+            // arrival and cursor are selected when a comparison needs them)
             int best = -1;
-            uint64_t bk = 0, ba = 0;
-            uint32_t bh = 0;
-            float bpf = 0.0f;
-            bool bex = true;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (harr[c] <= st.clock && (!blocked || ((st.flags >> c) & 1u))) {
                     bool better = best < 0;
                     if (!better) {
-                        const float d = pf[c] - bpf;
+                        const float d = pf[c] - sel3(best, pf);
                         if (use_bound && d > 2.5e-4f) {
                             better = true;
                         } else if (use_bound && d < -2.5e-4f) {
@@ -586,34 +477,24 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                                 key[c] = exact_key(kp, c, st.clock - harr[c]);
                                 ex[c] = true;
                             }
-                            if (!bex) {
 #pragma unroll
-                                for (int q = 0; q < c; ++q) {
-                                    if (q == best) {
-                                        key[q] = exact_key(kp, q, st.clock - harr[q]);
-                                        ex[q] = true;
-                                        bk = key[q];
-                                    }
+                            for (int q = 0; q < c; ++q) {
+                                if (q == best && !ex[q]) {
+                                    key[q] = exact_key(kp, q, st.clock - harr[q]);
+                                    ex[q] = true;
                                 }
-                                bex = true;
                             }
+                            const uint64_t bk = sel3(best, key), ba = sel3(best, harr);
                             better = key[c] > bk ||
                                      (key[c] == bk && (harr[c] < ba || (harr[c] == ba && [&] {
                                          uint32_t ic, ib, o, il;   // equal key and arrival: id order (R4)
                                          ld_inl_id_out(rec + st.head[c], il, ic, o);
-                                         ld_inl_id_out(rec + bh, il, ib, o);
+                                         ld_inl_id_out(rec + sel3(best, st.head), il, ib, o);
                                          return ic < ib;
                                      }())));
                         }
                     }
-                    if (better) {
-                        best = c;
-                        bk = key[c];
-                        bex = ex[c];
-                        bpf = pf[c];
-                        ba = harr[c];
-                        bh = st.head[c];
-                    }
+                    if (better) best = c;
                 }
             }
             if (best < 0) break;
@@ -689,7 +570,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 }
             }
         }
-        arm = tok == 0 && blocked;
         FSTAT(5, 1);
         FSTAT(12, tok == 0);
         FSTAT(13, ncomp == 0 && inl_sum == 0 && tok > 0);
