@@ -211,6 +211,16 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
     auto bound_dyn = [&](int c, uint64_t w) -> float {     // c not known at compile time
         return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? fS(c) : k1_filter_f32(fS(c), fp2(c), fC2(c), w);
     };
+    // A window of j iterations of length dt stops at the first iteration that ingests the next
+    // arrival: min(j, ceil((next_arr - clock) / dt)).  The 64-bit division is needed only when the
+    // window's last iteration starts at or after the arrival (else the quotient is >= j).
+    auto arr_cap = [&](uint64_t j, uint64_t dt) -> uint64_t {
+        if (next_arr != ~0ull && st.clock + (j - 1) * dt >= next_arr) {
+            const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
+            j = ja < j ? ja : j;
+        }
+        return j;
+    };
 
     for (;;) {
         // ---- a1: arrivals <= clock join the pending set (their class queue already holds them)
@@ -237,11 +247,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             const uint64_t F = cal.next;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = F - st.iter;
-            if (next_arr != ~0ull) {
-                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
-                j = ja < j ? ja : j;
-            }
             j = j < budget ? j : budget;
+            j = arr_cap(j, dt);
             FSTAT(1, 1);
             FSTAT(6, st.iter + j == F);
             FSTAT(11, j);
@@ -270,6 +277,10 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             for (int c = 0; c < 3; ++c)
                 if (harr[c] <= st.clock && (((st.flags >> c) & 1u) || (uint64_t)hf[c] <= st.kv_free)) stuck = false;
         }
+        // FP32 bounds of the pending heads now: shared by L4c, L5 and the scan's ordering
+        float pf[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pf[c] = (!stuck && prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
         // L4c: some head that does not fit ranks, *now*, above every head that fits even at the
         // start of the window's last iteration.  Priorities only grow with waiting time (L1), so
         // at every iteration of the window the top-ranked head misfits and blocks all admissions
@@ -281,11 +292,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             FSTAT(10, 1);
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = cal.next - st.iter;
-            if (next_arr != ~0ull) {
-                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
-                j = ja < j ? ja : j;
-            }
             j = j < budget ? j : budget;
+            j = arr_cap(j, dt);
             bool zero_head = false;
             float ptop = -1.0f;
 #pragma unroll
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 const bool pend = harr[c] <= st.clock;
                 zero_head |= pend && ((zmask >> c) & 1u);
                 if (pend && !((zmask >> c) & 1u) && (uint64_t)hf[c] > st.kv_free) {
-                    const float p = bound(c, st.clock - harr[c]);
+                    const float p = pf[c];
                     ptop = p > ptop ? p : ptop;
                 }
             }
@@ -332,12 +340,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             const uint64_t F = cal.next;
             const uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint64_t j = F - st.iter;
-            if (next_arr != ~0ull) {
-                const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
-                j = ja < j ? ja : j;
-            }
             j = j < budget ? j : budget;
             j = j < l4c_j ? j : l4c_j;
+            j = arr_cap(j, dt);
 #ifdef TCM_VAR_FSTATS
             {
                 FSTAT(l4c_j == ~0ull ? 2 : 3, 1);
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             for (int c = 0; c < 3; ++c) {
                 if (harr[c] <= st.clock && (((st.flags >> c) & 1u) || (uint64_t)hf[c] <= st.kv_free)) {
                     cand |= 1u << c;
-                    const float p = prio ? bound(c, st.clock - harr[c]) : 0.0f;
+                    const float p = pf[c];
                     if (top < 0 || p > ptop) {
                         top = c;
                         ptop = p;
@@ -393,11 +398,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                 uint64_t j = (rt - 1) / left;                   // rem stays > 0
                 const uint64_t jf = F - st.iter;
                 j = jf < j ? jf : j;
-                if (next_arr != ~0ull) {
-                    const uint64_t ja = (next_arr - st.clock + dt - 1) / dt;
-                    j = ja < j ? ja : j;
-                }
                 j = j < budget ? j : budget;
+                j = arr_cap(j, dt);
                 cand &= ~(1u << top);
                 bool ok = j >= 1;
                 if (prio && cand) {
@@ -448,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         const uint64_t it1 = st.iter + 1;                   // this iteration's number
         bool blocked = false;                               // R6
         uint64_t key[3];
-        float pf[3];          // FP32 bound of each head's priority (|P~ - P| <= 1e-5)
         bool ex[3];           // ex[c]: key[c] holds the exact K1 key
         // Two heads whose bounds are more than 2.5e-4 apart are ordered by the bounds (the exact
         // order, since the bound error is < 1e-5); only closer pairs get their exact FP64 keys.
@@ -456,7 +457,6 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
         for (int c = 0; c < 3; ++c) {
             key[c] = 0;
             ex[c] = !prio;
-            pf[c] = (prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
         }
         while (left > 0) {
             // tournament over the eligible heads carrying only the leader's index (its bound, key,
