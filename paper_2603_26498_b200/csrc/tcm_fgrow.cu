@@ -106,7 +106,6 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
         return (w == 0 || ((zmask >> c) & 1u) || !use_bound) ? s_fc[0][c][tid]
                                                               : k1_filter_f32(s_fc[0][c][tid], s_fc[1][c][tid], s_fc[2][c][tid], w);
     };
-    bool arm = false;     // the previous decision was blocked: try L4c
 
     // the head of class c: the top of its preempted stack, else the segment cursor.  hpos = its
     // position, harr its arrival (~0: none yet / exhausted), hneed the KV it reserves when admitted
@@ -218,9 +217,8 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
             // Lemma L4c under growth (TCM): a head that does not fit ranks, now, above every head that fits
             // even at the start of the window's last iteration -- priorities only grow (L1) and the fitting
             // set only shrinks as the free KV does -- so every iteration of the window is blocked (R6).  FP32
-            // bounds with a 2.5e-4 margin, halving the window up to 6 times, after a blocked decision.
-            if (!stuck && arm && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
-                arm = false;
+            // bounds with a 2.5e-4 margin; tried before every decision with a misfitting head and no partial.
+            if (!stuck && prio && use_bound && st.n_dec > 0 && (st.flags & 7u) == 0) {
                 uint64_t j = jcap;
                 bool zero_head = false;
                 float ptop = -1.0f;
@@ -233,8 +231,11 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                         ptop = pb > ptop ? pb : ptop;
                     }
                 }
-                for (int h = 0; h < 6 && j >= 2 && !zero_head && ptop >= 0.0f; ++h, j >>= 1) {
-                    const uint64_t t_end = st.clock + (j - 1) * dt;
+                // as k_fused: the full window, then this decision alone (blocked: decided without the
+                // scan), then halvings >= 2, the first success taken
+                uint64_t cand = j, win = ~0ull;
+                for (int step = 0; step < 7 && cand >= 1 && !zero_head && ptop >= 0.0f; ++step) {
+                    const uint64_t t_end = st.clock + (cand - 1) * dt;
                     float pfit = -1.0f;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
@@ -243,11 +244,23 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                             pfit = pb > pfit ? pb : pfit;
                         }
                     }
-                    if (ptop - pfit > 2.5e-4f) {
-                        stuck = true;
-                        jcap = j;
-                        break;
+                    const bool ok = ptop - pfit > 2.5e-4f;
+                    if (step == 1) {
+                        if (!ok) break;
+                        win = 1;
+                        cand = j >> 1;
+                    } else {
+                        if (ok) {
+                            win = cand;
+                            break;
+                        }
+                        cand = step == 0 ? (cand == 1 ? 0 : 1) : cand >> 1;
                     }
+                    if (step >= 1 && cand < 2) break;
+                }
+                if (win != ~0ull) {
+                    stuck = true;
+                    jcap = win;
                 }
             }
             // Lemma L5 under growth: a reserved (partial) head that needs more than this iteration's budget
@@ -319,7 +332,6 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
                     if (c == tokc) st.rem[c] -= (uint32_t)(j * tokj);
-                if (tokj == 0) arm = true;                        // still blocked: try L4c again next
                 s_dec[tid] += j;
                 s_sum[tid] += j * st.n_pend;
                 s_maxp[tid] = st.n_pend > s_maxp[tid] ? st.n_pend : s_maxp[tid];
@@ -413,35 +425,50 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
         bool blocked = false;
         uint64_t key[3];
         bool ex[3];
+        // bound-first ordering as in k_fused: heads whose FP32 bounds differ by more than 2.5e-4 are
+        // ordered by them (|P~ - P| < 1e-5), closer pairs by the exact keys
+        float pf[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             key[c] = 0;
             ex[c] = !prio;
+            pf[c] = (prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
         }
         while (left > 0) {
             int best = -1;
-            uint64_t bk = 0, ba = 0;
-            uint32_t bp = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (harr[c] <= st.clock && (!blocked || ((st.flags >> c) & 1u))) {
-                    if (!ex[c]) {
-                        key[c] = exact_key(kp, c, st.clock - harr[c]);
-                        ex[c] = true;
+                    bool better = best < 0;
+                    if (!better) {
+                        const float d = pf[c] - sel3(best, pf);
+                        if (use_bound && d > 2.5e-4f) {
+                            better = true;
+                        } else if (use_bound && d < -2.5e-4f) {
+                            better = false;
+                        } else {
+                            if (!ex[c]) {
+                                key[c] = exact_key(kp, c, st.clock - harr[c]);
+                                ex[c] = true;
+                            }
+#pragma unroll
+                            for (int q = 0; q < c; ++q) {
+                                if (q == best && !ex[q]) {
+                                    key[q] = exact_key(kp, q, st.clock - harr[q]);
+                                    ex[q] = true;
+                                }
+                            }
+                            const uint64_t bk = sel3(best, key), ba = sel3(best, harr);
+                            better = key[c] > bk ||
+                                     (key[c] == bk && (harr[c] < ba || (harr[c] == ba && [&] {
+                                         uint32_t i1, i2, x, y;   // equal key and arrival: id order (R4)
+                                         ld_inl_id_out(rec + hpos[c], x, i1, y);
+                                         ld_inl_id_out(rec + sel3(best, hpos), x, i2, y);
+                                         return i1 < i2;
+                                     }())));
+                        }
                     }
-                    bool better = best < 0 || key[c] > bk ||
-                                  (key[c] == bk && (harr[c] < ba || (harr[c] == ba && [&] {
-                                      uint32_t i1, i2, x, y;   // equal key and arrival: id order (R4)
-                                      ld_inl_id_out(rec + hpos[c], x, i1, y);
-                                      ld_inl_id_out(rec + bp, x, i2, y);
-                                      return i1 < i2;
-                                  }())));
-                    if (better) {
-                        best = c;
-                        bk = key[c];
-                        ba = harr[c];
-                        bp = hpos[c];
-                    }
+                    if (better) best = c;
                 }
             }
             if (best < 0) break;
@@ -514,11 +541,11 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                         else st.head[c]++;                       // advance the segment cursor
                         load_head(c);
                         ex[c] = !prio;
+                        pf[c] = (prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
                     }
                 }
             }
         }
-        arm = tok == 0 && blocked;
         if (tok == 0 && st.n_dec == 0) {                   // unreachable under R6
             t.state[r].status = ST_DEADLOCK;
             st.flags |= FLAG_FINISHED;
