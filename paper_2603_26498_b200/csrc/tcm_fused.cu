@@ -313,16 +313,11 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
             for (int step = 0; step < 7 && cand >= 1 && !zero_head && ptop >= 0.0f; ++step) {
                 const uint64_t t_end = st.clock + (cand - 1) * dt;
                 float pfit = -1.0f;
-#ifndef TCM_FUSED_PFNOW
-#define TCM_FUSED_PFNOW 0
-#endif
-#if TCM_FUSED_PFNOW
                 if (cand == 1) {             // the window's end is now: the pass's bounds
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
                         if (harr[c] <= st.clock && (uint64_t)hf[c] <= st.kv_free) pfit = pf[c] > pfit ? pf[c] : pfit;
                 } else
-#endif
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     if (harr[c] <= st.clock && (uint64_t)hf[c] <= st.kv_free) {
@@ -417,13 +412,11 @@ __global__ void __launch_bounds__(kThreads, 8) k_fused(ModelConst m, TraceDev t,
                     for (int h = 0; h < 6 && j >= 1; ++h, j >>= 1) {
                         const uint64_t t_end = st.clock + (j - 1) * dt;
                         float pmax = -1.0f;
-#if TCM_FUSED_PFNOW
-                        if (j == 1) {
+                        if (j == 1) {            // the window's end is now: the pass's bounds
 #pragma unroll
                             for (int c = 0; c < 3; ++c)
                                 if ((cand >> c) & 1u) pmax = pf[c] > pmax ? pf[c] : pmax;
                         } else
-#endif
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             if ((cand >> c) & 1u) {
