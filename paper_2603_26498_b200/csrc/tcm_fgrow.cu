@@ -131,12 +131,32 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
 
     // R29's victim of class c: its newest running request, or NIL.  The reserved head is newer
     // than every decoding request of its class; otherwise scan down from the segment cursor.
+    // Scan cache per class: every position in [s_kT, s_kH) below the cursor is known not to be
+    // running (finished, or preempted and waiting).  A search scans the positions admitted since
+    // (s_kH .. cursor), then continues below s_kT; a victim that is re-admitted and decodes again at a
+    // position inside the known range shrinks it (see the scan).  Without it every preemption
+    // re-walked the finished and preempted positions under the cursor (22 % of k_fgrow's instructions).
+    __shared__ uint32_t s_kT[3][kGThreads], s_kH[3][kGThreads];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s_kT[c][tid] = s_kH[c][tid] = s_seg[c][tid];
     auto newest_running = [&](int c) -> uint32_t {
         if ((st.flags >> c) & 1u) return hpos[c];
         const uint32_t s0 = s_seg[c][tid];
-        for (uint32_t q = st.head[c]; q > s0; --q)
-            if (pfin[q - 1] > st.iter) return q - 1;
-        return NIL;
+        uint32_t found = NIL;
+        for (uint32_t q = st.head[c]; q > s_kH[c][tid]; --q)
+            if (pfin[q - 1] > st.iter) {
+                found = q - 1;
+                break;
+            }
+        if (found == NIL)
+            for (uint32_t q = s_kT[c][tid]; q > s0; --q)
+                if (pfin[q - 1] > st.iter) {
+                    found = q - 1;
+                    break;
+                }
+        s_kT[c][tid] = found == NIL ? s0 : found + 1;
+        s_kH[c][tid] = st.head[c];
+        return found;
     };
 
     for (;;) {
@@ -523,6 +543,9 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                         const uint32_t kvF = res + (o - gen);
                         fin(id) = F;
                         pfin[p] = F;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)      // running again inside a known-idle range
+                            if (c == best && p >= s_kT[c][tid] && p < s_kH[c][tid]) s_kT[c][tid] = p + 1;
                         pkv[p] = kvF;
                         cal.insert(F, kvF);
                         new_dec++;
