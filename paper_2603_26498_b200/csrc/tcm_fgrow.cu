@@ -118,10 +118,14 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
         const uint32_t p = tp != NIL ? tp : st.head[c];
         uint64_t a;
         uint32_t f;
+        // the flag and the remainder are loaded with the record (positions are valid up to the
+        // sentinels), so the three loads are in flight together
+        const uint8_t fl = pflag[p];
+        const uint32_t pr = prem[p];
         ld_arrfp(rec + p, a, f);
         hpos[c] = p;
         harr[c] = a;
-        hneed[c] = (a != ~0ull && (pflag[p] & PF_PREV)) ? prem[p] : f;
+        hneed[c] = (a != ~0ull && (fl & PF_PREV)) ? pr : f;
     };
 #pragma unroll
     for (int c = 0; c < 3; ++c) load_head(c);
@@ -206,6 +210,10 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
         // ---- closed-form windows with pending requests (no preemption due: kv_free >= n_dec).  Each
         // iteration of a window charges n_dec decode tokens, so it lasts at most kv_free / n_dec
         // iterations (R28), and ends at the next finish or arrival.
+        // FP32 bounds of the pending heads now, shared by L4c, L5 and (no preemption happens in a pass
+        // whose window section ran: kv_free >= n_dec) the scan's ordering
+        float pf[3];
+        bool pf_ok = false;
         if (st.n_pend > 0 && st.kv_free >= st.n_dec) {
             const uint32_t left0 = B > st.n_dec ? B - st.n_dec : 0;   // R8
             const uint64_t kv_after = st.kv_free - st.n_dec;          // free KV once this iteration's tokens are charged
@@ -227,6 +235,11 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                 for (int c = 0; c < 3; ++c)
                     if (harr[c] <= st.clock && (uint64_t)hneed[c] <= kv_after) stuck = false;
             }
+            if (!stuck && prio) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) pf[c] = harr[c] <= st.clock ? bound(c, st.clock - harr[c]) : 0.0f;
+                pf_ok = true;
+            }
             uint64_t dt = m.c0 + m.cd * st.n_dec;
             uint32_t tokj = 0;
             int tokc = 0;                                 // the class whose partial head takes the tokens
@@ -247,7 +260,7 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                     const bool pend = harr[c] <= st.clock;
                     zero_head |= pend && ((zmask >> c) & 1u);
                     if (pend && !((zmask >> c) & 1u) && (uint64_t)hneed[c] > kv_after) {
-                        const float pb = bound(c, st.clock - harr[c]);
+                        const float pb = pf[c];
                         ptop = pb > ptop ? pb : ptop;
                     }
                 }
@@ -257,6 +270,11 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                 for (int step = 0; step < 7 && cand >= 1 && !zero_head && ptop >= 0.0f; ++step) {
                     const uint64_t t_end = st.clock + (cand - 1) * dt;
                     float pfit = -1.0f;
+                    if (cand == 1) {             // the window's end is now: the pass's bounds
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            if (harr[c] <= st.clock && (uint64_t)hneed[c] <= kv_after) pfit = pf[c] > pfit ? pf[c] : pfit;
+                    } else
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         if (harr[c] <= st.clock && (uint64_t)hneed[c] <= kv_after) {
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                 for (int c = 0; c < 3; ++c) {
                     if (harr[c] <= st.clock && (((st.flags >> c) & 1u) || (uint64_t)hneed[c] <= kv_after)) {
                         cand |= 1u << c;
-                        const float pb = prio ? bound(c, st.clock - harr[c]) : 0.0f;
+                        const float pb = prio ? pf[c] : 0.0f;
                         if (top < 0 || pb > ptop) {
                             top = c;
                             ptop = pb;
@@ -322,6 +340,11 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
                         for (int h = 0; h < 6 && j >= 1; ++h, j >>= 1) {
                             const uint64_t t_end = st.clock + (j - 1) * dt5;
                             float pmax = -1.0f;
+                            if (j == 1) {
+#pragma unroll
+                                for (int c = 0; c < 3; ++c)
+                                    if ((cand >> c) & 1u) pmax = pf[c] > pmax ? pf[c] : pmax;
+                            } else
 #pragma unroll
                             for (int c = 0; c < 3; ++c) {
                                 if ((cand >> c) & 1u) {
@@ -447,12 +470,11 @@ __global__ void __launch_bounds__(kGThreads, 8) k_fgrow(ModelConst m, TraceDev t
         bool ex[3];
         // bound-first ordering as in k_fused: heads whose FP32 bounds differ by more than 2.5e-4 are
         // ordered by them (|P~ - P| < 1e-5), closer pairs by the exact keys
-        float pf[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             key[c] = 0;
             ex[c] = !prio;
-            pf[c] = (prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
+            if (!pf_ok) pf[c] = (prio && harr[c] <= st.clock) ? bound(c, st.clock - harr[c]) : 0.0f;
         }
         while (left > 0) {
             int best = -1;
