@@ -4,7 +4,7 @@ set -u
 mkdir -p gpurun_out/sanitizer
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
 for tool in ${TOOLS:-racecheck synccheck initcheck memcheck}; do
-  for mode in ${MODES:-fused step1 step8 cluster growth edf}; do
+  for mode in ${MODES:-fused step1 step1tcm step8 cluster growth edf fgrow}; do
     size=""
     if [ $tool = racecheck ]; then size="4 200"; [ $mode = cluster ] && size="1 600"; fi
     timeout ${PER:-420} compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize_run.py $mode $size \
