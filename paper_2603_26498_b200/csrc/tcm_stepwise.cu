@@ -57,6 +57,9 @@ constexpr uint8_t RS_DEC = 32, RS_PREV = 64, RS_GEN = 128;
 #ifndef TCM_SW_MINB
 #define TCM_SW_MINB 3
 #endif
+#ifndef TCM_SW_GRMINB
+#define TCM_SW_GRMINB 2      // NEXT-1 instantiations: 2 blocks / SM, 128 registers, no spills
+#endif
 constexpr int kStages = TCM_SW_STAGES;
 constexpr size_t kRingBytes = (size_t)kWarpsPerBlock * kStages * (128 * 8 + 32 * 4);
 
@@ -596,7 +599,7 @@ __device__ __noinline__ uint64_t sw_edf_invert(const TraceDev& t, uint32_t r, ui
 // TO: every replica runs plain TCM (TraceDev.all_tcm): the FCFS / EDF / first-fit paths compile out
 // (a smaller kernel for the instruction cache).
 template <int G, bool GR, int CL, bool TO = false>
-__global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : TCM_SW_MINB) k_step(ModelConst m, TraceDev t, uint32_t* remv,
+__global__ void __launch_bounds__(kThreads, CL > 1 ? 1 : (GR ? TCM_SW_GRMINB : TCM_SW_MINB)) k_step(ModelConst m, TraceDev t, uint32_t* remv,
                                                                              StepCtl ctl) {
     constexpr int kGroups = kWarpsPerBlock / G;
     constexpr int kMaxDone = GroupSmem<G>::kMaxDone;
@@ -1347,6 +1350,7 @@ constexpr int kCluster = 8;    // CTAs per replica for a few huge queues (portab
 // Per-device launch facts, queried once (kernel attributes and occupancy do not change).
 struct DevFacts {
     int sms = 0, per_sm1 = 1, per_sm8 = 1;
+    int per_sm1g = 1, per_sm8g = 1;     // the NEXT-1 instantiations (2 blocks / SM: no spills)
 };
 
 DevFacts dev_facts() {
@@ -1371,6 +1375,10 @@ DevFacts dev_facts() {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p8, k_step<8, false, 1>, kThreads, kRingBytes);
         f.per_sm1 = p1 < 1 ? 1 : p1;
         f.per_sm8 = p8 < 1 ? 1 : p8;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_step<1, true, 1>, kThreads, kRingBytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p8, k_step<8, true, 1>, kThreads, kRingBytes);
+        f.per_sm1g = p1 < 1 ? 1 : p1;
+        f.per_sm8g = p8 < 1 ? 1 : p8;
         f.sms = sms;
     }
     return f;
@@ -1385,9 +1393,9 @@ bool use_to() {
     return on;
 }
 
-Launch stepwise_config(uint32_t R, uint64_t N) {
+Launch stepwise_config(uint32_t R, uint64_t N, bool growth) {
     const DevFacts f = dev_facts();
-    const int sms = f.sms, per_sm1 = f.per_sm1, per_sm8 = f.per_sm8;
+    const int sms = f.sms, per_sm1 = growth ? f.per_sm1g : f.per_sm1, per_sm8 = growth ? f.per_sm8g : f.per_sm8;
     // Warp per replica unless the queues are few and huge: a CTA per replica only when there are
     // fewer replicas than twice the warp slots AND they average >= 8,192 requests (measured: for
     // sweeps of ~1k-request replicas a warp per replica is 2.2x faster, its iterations need no
@@ -1441,7 +1449,7 @@ tcm_status stepwise_run(const ModelConst& m, const TraceDev& t, const StepwiseWo
                         uint32_t* active_out, cudaStream_t s, uint64_t* launches, cudaEvent_t ev_begin,
                         cudaEvent_t ev_end, double* kernel_ms, bool* deferred) {
     uint32_t* remv = reinterpret_cast<uint32_t*>(w.base);
-    const Launch L = stepwise_config(t.R, t.N);
+    const Launch L = stepwise_config(t.R, t.N, t.any_growth != 0);
     StepCtl ctl{};
     ctl.w = w.sync;
     ctl.dyn = L.group == 1 && L.cluster == 1 && t.R > (uint64_t)L.grid * kWarpsPerBlock;   // else static is ideal
