@@ -228,6 +228,21 @@ tcm_status tcm_step(tcm_ctx* ctx, uint32_t max_iterations, uint32_t* active_repl
  * hit its deadlock assertion. */
 tcm_status tcm_run(tcm_ctx* ctx);
 
+/* tcm_run without waiting (FUSED engine only, TCM_E_ARG otherwise): enqueues the engine to
+ * completion, the first-token / finish stamping and, for HOST results, their device-to-host copy
+ * on the context's stream, and returns.  A pipeline of contexts overlaps one context's copies with
+ * another's kernels: tcm_wait(ctx, TCM_WAIT_ENGINE) returns once the kernels are done (the copy
+ * may still run), tcm_wait(ctx, TCM_WAIT_ALL) once everything is, and then reports what tcm_run
+ * would (TCM_E_REPLICA on a deadlock assertion).  The copy-back runs on a stream of the library's own
+ * after the kernels, so tcm_stats may be called as soon as the call returns (its kernels follow the
+ * engine on the context's stream; its *_ms fields count the run only after TCM_WAIT_ALL).  The HOST
+ * results are valid after TCM_WAIT_ALL; tcm_load_trace / tcm_reset / tcm_step / tcm_run /
+ * tcm_run_async before it are TCM_E_STATE. */
+#define TCM_WAIT_ENGINE 0
+#define TCM_WAIT_ALL 1
+tcm_status tcm_run_async(tcm_ctx* ctx);
+tcm_status tcm_wait(tcm_ctx* ctx, int what);
+
 /* Fills *out (may be NULL) and, when dev_hist / dev_cnt are non-NULL, writes the a6
  * aggregation: dev_hist[n_cells][4][496] and dev_cnt[n_cells][4][6] (int64, DEVICE,
  * overwritten; groups M, C, T, all; counters n, sum TTFT, sum E2E, SLO violations,

@@ -30,11 +30,13 @@ struct tcm_ctx {
     tcm_results_view host_res{};
     uint32_t* d_active = nullptr;        // [1]
     unsigned long long* d_acc = nullptr; // [kAccN]
-    uint32_t* d_val = nullptr;           // [3] worst status, first bad replica, any TCM_KV_GROWTH
+    uint32_t* d_val = nullptr;           // [3] worst status, first bad replica, any TCM_KV_GROWTH (16 bytes)
     StepwiseWorkspace sw{};
     uint64_t launches = 0;
     // device timing of the library's launches (tcm_stats_host.*_ms)
-    cudaEvent_t ev[7] = {};              // reset begin/end, engine begin/end, stamp end, k_step begin/end
+    cudaEvent_t ev[9] = {};              // reset begin/end, engine begin/end, stamp end, k_step begin/end,
+                                         // tcm_run_async: engine done, results copied
+    bool async_pending = false;          // a tcm_run_async not yet completed by tcm_wait(TCM_WAIT_ALL)
     bool reset_pending = false;          // ev[0..1] recorded, not yet read
     double reset_ms = 0, engine_ms = 0, stamp_ms = 0;
     // tcm_step(n <= kGraphMaxIters): the call's launches (k_step, or k_fused + stamp with the
@@ -46,6 +48,9 @@ struct tcm_ctx {
     std::vector<uint32_t> graph_never;   // n whose capture failed: always eager
     uint32_t* h_active = nullptr;        // pinned: the graphs' active-count target
     uint32_t* h_active_dev = nullptr;    // its mapped device address (stepwise graphs: k_step writes it)
+    unsigned long long* h_acc = nullptr; // pinned mapped copy of the k_reduce accumulators
+    unsigned long long* h_acc_dev = nullptr;
+    cudaStream_t xs = nullptr;           // tcm_run_async's copy-back stream (after the engine's event)
     cudaStream_t cs = nullptr;           // capture stream (the caller's may be the legacy stream,
                                          // which cannot be captured; a graph launches into any stream)
 };
@@ -169,19 +174,20 @@ size_t ws_bytes(const tcm_config* cfg, uint32_t R, uint64_t N, int host_mirror) 
     return b;
 }
 
-tcm_status copy_results_to_host(tcm_ctx* c) {
+tcm_status copy_results_to_host(tcm_ctx* c, cudaStream_t s = nullptr) {
     if (!c->host_results) return TCM_OK;
+    if (!s) s = c->s;
     const uint64_t N = c->t.N;
     if (c->host_res.admit_seq)
-        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.admit_seq, c->t.admit_seq, 4 * N, cudaMemcpyDeviceToHost, c->s));
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.admit_seq, c->t.admit_seq, 4 * N, cudaMemcpyDeviceToHost, s));
     if (c->host_res.first_token_us)
-        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.first_token_us, c->t.first_token, 8 * N, cudaMemcpyDeviceToHost, c->s));
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.first_token_us, c->t.first_token, 8 * N, cudaMemcpyDeviceToHost, s));
     if (c->host_res.done_us)
-        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.done_us, c->t.done, 8 * N, cudaMemcpyDeviceToHost, c->s));
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.done_us, c->t.done, 8 * N, cudaMemcpyDeviceToHost, s));
     if (c->host_res.preempt_count && c->t.pcount)
-        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.preempt_count, c->t.pcount, 4 * N, cudaMemcpyDeviceToHost, c->s));
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.preempt_count, c->t.pcount, 4 * N, cudaMemcpyDeviceToHost, s));
     if (c->host_res.preempted_us && c->t.ptime)
-        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.preempted_us, c->t.ptime, 8 * N, cudaMemcpyDeviceToHost, c->s));
+        TCM_CUDA(c, cudaMemcpyAsync(c->host_res.preempted_us, c->t.ptime, 8 * N, cudaMemcpyDeviceToHost, s));
     return TCM_OK;
 }
 
@@ -191,6 +197,13 @@ tcm_status reduce_stats(tcm_ctx* c, unsigned long long* h) {
     launch_reduce(c->t, c->d_acc, c->s);
     c->launches++;
     TCM_CUDA(c, cudaGetLastError());
+    if (c->h_acc_dev) {                  // stores into mapped memory: never waits behind a copy-back in flight
+        launch_copy_words(c->d_acc, c->h_acc_dev, kAccN, c->s);
+        c->launches++;
+        TCM_CUDA(c, cudaStreamSynchronize(c->s));
+        memcpy(h, c->h_acc, kAccN * 8);
+        return TCM_OK;
+    }
     TCM_CUDA(c, cudaMemcpyAsync(h, c->d_acc, kAccN * 8, cudaMemcpyDeviceToHost, c->s));
     TCM_CUDA(c, cudaStreamSynchronize(c->s));
     return TCM_OK;
@@ -374,14 +387,19 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
     cudaError_t e = cudaGetDevice(&c->device);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_active, 4);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_acc, kAccN * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 12);
-    for (int i = 0; i < 7 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_val, 16);
+    for (int i = 0; i < 9 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     if (e == cudaSuccess && cudaMallocHost(&c->h_active, 4) != cudaSuccess) {
         c->h_active = nullptr;                      // no pinned word: short calls run eagerly
         cudaGetLastError();
     }
     if (c->h_active && cudaHostGetDevicePointer((void**)&c->h_active_dev, c->h_active, 0) != cudaSuccess) {
         c->h_active_dev = nullptr;                  // not mapped: the graph copies the count instead
+        cudaGetLastError();
+    }
+    if (e == cudaSuccess && (cudaMallocHost(&c->h_acc, kAccN * 8) != cudaSuccess ||
+                             cudaHostGetDevicePointer((void**)&c->h_acc_dev, c->h_acc, 0) != cudaSuccess)) {
+        c->h_acc_dev = nullptr;                     // the stats read back with a copy instead
         cudaGetLastError();
     }
     if (e != cudaSuccess) {
@@ -400,6 +418,7 @@ tcm_status tcm_create(const tcm_config* cfg, void* cuda_stream, tcm_ctx** out) {
 
 tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_results_view* rv) {
     if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (c->async_pending) return fail(c, TCM_E_STATE, "tcm_load_trace while a tcm_run_async is pending (tcm_wait first)");
     if (!tv) return fail(c, TCM_E_ARG, "trace is NULL");
     if (tv->n_replicas == 0) return fail(c, TCM_E_ARG, "n_replicas must be >= 1");
     if (!tv->req_offset || !tv->params || (tv->n_requests > 0 && (!tv->arrival_us || !tv->footprint ||
@@ -521,8 +540,15 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
     launch_validate(t, c->d_val, c->cfg.engine == TCM_ENGINE_STEPWISE, s);
     c->launches++;
     TCM_CUDA(c, cudaGetLastError());
-    TCM_CUDA(c, cudaMemcpyAsync(hv, c->d_val, 12, cudaMemcpyDeviceToHost, s));
-    TCM_CUDA(c, cudaStreamSynchronize(s));
+    if (c->h_acc_dev) {                  // through mapped memory (see reduce_stats)
+        launch_copy_words(reinterpret_cast<const unsigned long long*>(c->d_val), c->h_acc_dev, 2, s);
+        c->launches++;
+        TCM_CUDA(c, cudaStreamSynchronize(s));
+        memcpy(hv, c->h_acc, 12);
+    } else {
+        TCM_CUDA(c, cudaMemcpyAsync(hv, c->d_val, 12, cudaMemcpyDeviceToHost, s));
+        TCM_CUDA(c, cudaStreamSynchronize(s));
+    }
     c->t.any_growth = t.any_growth = hv[2] & 1u;
     c->t.all_growth = t.all_growth = (hv[2] & 2u) == 0;
     c->t.all_tcm = t.all_tcm = (hv[2] & 4u) == 0;
@@ -579,12 +605,14 @@ tcm_status tcm_load_trace(tcm_ctx* c, const tcm_trace_view* tv, const tcm_result
 
 tcm_status tcm_reset(tcm_ctx* c) {
     if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (c->async_pending) return fail(c, TCM_E_STATE, "tcm_reset while a tcm_run_async is pending (tcm_wait first)");
     if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_reset before tcm_load_trace");
     return reset_state(c);
 }
 
 tcm_status tcm_step(tcm_ctx* c, uint32_t max_iterations, uint32_t* active_replicas) {
     if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (c->async_pending) return fail(c, TCM_E_STATE, "tcm_step while a tcm_run_async is pending (tcm_wait first)");
     if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_step before tcm_load_trace");
     uint32_t active = 0;
     tcm_status st = run_engine(c, max_iterations, &active);
@@ -599,6 +627,7 @@ tcm_status tcm_step(tcm_ctx* c, uint32_t max_iterations, uint32_t* active_replic
 
 tcm_status tcm_run(tcm_ctx* c) {
     if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (c->async_pending) return fail(c, TCM_E_STATE, "tcm_run while a tcm_run_async is pending (tcm_wait first)");
     if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_run before tcm_load_trace");
     uint32_t active = 1;
     while (active > 0) {
@@ -610,6 +639,60 @@ tcm_status tcm_run(tcm_ctx* c) {
     if (st != TCM_OK) return st;
     if ((st = copy_results_to_host(c)) != TCM_OK) return st;
     TCM_CUDA(c, cudaStreamSynchronize(c->s));
+    if (h[kAccBadStatus] != 0)
+        return fail(c, TCM_E_REPLICA, "replica %llu reported status %llu (deadlock assertion)",
+                    h[kAccBadReplica], h[kAccBadStatus]);
+    return TCM_OK;
+}
+
+tcm_status tcm_run_async(tcm_ctx* c) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (!c->loaded) return fail(c, TCM_E_STATE, "tcm_run_async before tcm_load_trace");
+    if (c->cfg.engine != TCM_ENGINE_FUSED) return fail(c, TCM_E_ARG, "tcm_run_async: FUSED engine only");
+    if (c->async_pending) return fail(c, TCM_E_STATE, "tcm_run_async: the previous run is still pending (tcm_wait)");
+    if (!c->h_active) return fail(c, TCM_E_STATE, "tcm_run_async: no pinned host word");
+    // one engine launch runs every replica to completion (the iteration budget never binds), then the
+    // stamping; the active count lands in the pinned word and is checked by tcm_wait
+    uint64_t l = 0;
+    bool deferred = false;
+    tcm_status st = enqueue_engine(c, 0xFFFFFFFFu, c->h_active, &l, &deferred);
+    c->launches += l;
+    if (st != TCM_OK) return st;
+    TCM_CUDA(c, cudaEventRecord(c->ev[7], c->s));
+    // the copy-back runs on a stream of its own once the kernels are done, so tcm_stats (kernels on
+    // the context's stream) need not wait for it
+    if (!c->xs) TCM_CUDA(c, cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking));
+    TCM_CUDA(c, cudaStreamWaitEvent(c->xs, c->ev[7], 0));
+    if ((st = copy_results_to_host(c, c->xs)) != TCM_OK) return st;
+    TCM_CUDA(c, cudaEventRecord(c->ev[8], c->xs));
+    c->async_pending = true;                 // load / reset / step / run wait for tcm_wait(TCM_WAIT_ALL)
+    return TCM_OK;
+}
+
+tcm_status tcm_wait(tcm_ctx* c, int what) {
+    if (!c) return fail(nullptr, TCM_E_ARG, "ctx is NULL");
+    if (what != TCM_WAIT_ENGINE && what != TCM_WAIT_ALL) return fail(c, TCM_E_ARG, "tcm_wait: bad what (%d)", what);
+    if (!c->async_pending) return TCM_OK;
+    if (what == TCM_WAIT_ENGINE) {
+        TCM_CUDA(c, cudaEventSynchronize(c->ev[7]));
+        return TCM_OK;
+    }
+    TCM_CUDA(c, cudaEventSynchronize(c->ev[8]));
+    c->async_pending = false;
+    float ms = 0;
+    if (c->reset_pending) {
+        TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+        c->reset_ms += ms;
+        c->reset_pending = false;
+    }
+    TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+    c->engine_ms += ms;
+    TCM_CUDA(c, cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
+    c->stamp_ms += ms;
+    if (*c->h_active != 0) return fail(c, TCM_E_STATE, "tcm_wait: %u replicas unfinished", *c->h_active);
+    unsigned long long h[kAccN];
+    tcm_status st = reduce_stats(c, h);
+    if (st != TCM_OK) return st;
     if (h[kAccBadStatus] != 0)
         return fail(c, TCM_E_REPLICA, "replica %llu reported status %llu (deadlock assertion)",
                     h[kAccBadReplica], h[kAccBadStatus]);
@@ -700,7 +783,9 @@ void tcm_destroy(tcm_ctx* c) {
     cudaFree(c->d_acc);
     cudaFree(c->d_val);
     if (c->h_active) cudaFreeHost(c->h_active);
+    if (c->h_acc) cudaFreeHost(c->h_acc);
     if (c->cs) cudaStreamDestroy(c->cs);
+    if (c->xs) cudaStreamDestroy(c->xs);
     delete c;
 }
 

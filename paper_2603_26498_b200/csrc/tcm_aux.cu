@@ -428,6 +428,12 @@ void launch_validate(const TraceDev& t, uint32_t* v, int general_ok, cudaStream_
 void launch_reduce(const TraceDev& t, unsigned long long* acc, cudaStream_t s) {
     k_reduce<<<(t.R + 255) / 256, 256, 0, s>>>(t, acc);
 }
+__global__ void k_copy_words(const unsigned long long* src, unsigned long long* dst, int n) {
+    if ((int)threadIdx.x < n) dst[threadIdx.x] = src[threadIdx.x];
+}
+void launch_copy_words(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s) {
+    k_copy_words<<<1, 32, 0, s>>>(src, dst, n);
+}
 void launch_aggregate(const ModelConst& m, const TraceDev& t, unsigned long long* hist,
                       unsigned long long* cnt, cudaStream_t s) {
     k_aggregate<<<(t.R + kAggTile - 1) / kAggTile, 256, 0, s>>>(m, t, hist, cnt);

@@ -18,6 +18,9 @@ void launch_preempt_stats(const ModelConst& m, const TraceDev& t, unsigned long 
 void launch_kpack(const ModelConst& m, const TraceDev& t, cudaStream_t s);
 void launch_validate(const TraceDev& t, uint32_t* v, int general_ok, cudaStream_t s);
 void launch_reduce(const TraceDev& t, unsigned long long* acc, cudaStream_t s);
+// n words device -> mapped host memory by plain stores (no copy-engine DMA: a small readback does not
+// queue behind a large copy in flight on another stream)
+void launch_copy_words(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s);
 void launch_aggregate(const ModelConst& m, const TraceDev& t, unsigned long long* hist,
                       unsigned long long* cnt, cudaStream_t s);
 void launch_generate(const void* reps, uint32_t R, const uint64_t* off, uint64_t* arrival,

@@ -27,7 +27,8 @@ MEM_DEVICE, MEM_HOST = 0, 1
 HIST_BINS, GROUPS, NCNT = 496, 4, 6
 INF32 = 0xFFFFFFFF
 
-EXPORTS = ("tcm_create", "tcm_load_trace", "tcm_reset", "tcm_step", "tcm_run", "tcm_stats", "tcm_destroy",
+EXPORTS = ("tcm_create", "tcm_load_trace", "tcm_reset", "tcm_step", "tcm_run", "tcm_run_async", "tcm_wait", "tcm_stats",
+           "tcm_destroy",
            "tcm_last_error", "tcm_workspace_bytes", "tcm_generate_trace", "tcm_k1_eval",
            "tcm_k1_audit", "tcm_k1_filter_error", "tcm_replica_counters", "tcm_preemption_stats")
 
@@ -101,6 +102,10 @@ def lib():
         L.tcm_step.argtypes = [vp, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]
         L.tcm_run.restype = st
         L.tcm_run.argtypes = [vp]
+        L.tcm_run_async.restype = st
+        L.tcm_run_async.argtypes = [vp]
+        L.tcm_wait.restype = st
+        L.tcm_wait.argtypes = [vp, ctypes.c_int]
         L.tcm_stats.restype = st
         L.tcm_stats.argtypes = [vp, ctypes.POINTER(tcm_stats_host), vp, vp]
         L.tcm_replica_counters.restype = st
@@ -207,6 +212,17 @@ def tcm_step(ctx, max_iterations: int) -> int:
 
 def tcm_run(ctx):
     _check(lib().tcm_run(ctx), ctx)
+
+
+WAIT_ENGINE, WAIT_ALL = 0, 1
+
+
+def tcm_run_async(ctx):
+    _check(lib().tcm_run_async(ctx), ctx)
+
+
+def tcm_wait(ctx, what: int = WAIT_ALL):
+    _check(lib().tcm_wait(ctx, what), ctx)
 
 
 def tcm_stats(ctx, dev_hist=None, dev_cnt=None) -> dict:
@@ -346,6 +362,12 @@ class Simulation:
 
     def run(self):
         tcm_run(self.ctx)
+
+    def run_async(self):
+        tcm_run_async(self.ctx)
+
+    def wait(self, what: int = WAIT_ALL):
+        tcm_wait(self.ctx, what)
 
     def reset(self):
         tcm_reset(self.ctx)

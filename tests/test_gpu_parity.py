@@ -169,6 +169,38 @@ def test_host_buffers_equal_device_buffers():
         np.testing.assert_array_equal(a[k], b[k])
 
 
+def test_run_async_equals_run():
+    """tcm_run_async + tcm_wait (the pipelined e2e path) gives tcm_run's results and counters, twice in a
+    row on one context; calls during a pending run are refused; the stepwise engine refuses the call."""
+    tr, params = sweep(48, 300, 37)
+    _, a, sa = run_gpu(tr, params, mem=tcm.MEM_HOST)
+    host = {"req_offset": tr.offset, "arrival_us": tr.arrival_us, "footprint": tr.footprint,
+            "inline_us": tr.inline_us, "out_tokens": tr.out_tokens, "modality": tr.modality, "params": params}
+    sim = tcm.Simulation(tcm.config(engine=tcm.ENGINE_FUSED))
+    for rep in range(2):
+        res = {k: np.zeros_like(v) for k, v in a.items()}
+        sim.load(host, res, mem=tcm.MEM_HOST)
+        sim.run_async()
+        with pytest.raises(tcm.TcmError):
+            sim.step(1)                                   # TCM_E_STATE while pending
+        sim.wait(tcm.WAIT_ENGINE)
+        sp = sim.stats()                                  # allowed before the copy-back is done
+        sim.wait(tcm.WAIT_ALL)
+        assert sp["decisions"] == sa["decisions"] and sp["requests_done"] == sa["requests_done"]
+        sim.wait(tcm.WAIT_ALL)                            # nothing pending: a no-op
+        for k in a:
+            np.testing.assert_array_equal(res[k], a[k], err_msg=f"rep {rep} {k}")
+        sb = sim.stats()
+        for k in ("iterations", "decisions", "sum_pending", "requests_done", "scanned_decisions"):
+            assert sb[k] == sa[k], k
+    sim.close()
+    sw = tcm.Simulation(tcm.config(engine=tcm.ENGINE_STEPWISE))
+    sw.load(tcm.to_device(tr, params), tcm.alloc_results(tr.n_requests))
+    with pytest.raises(tcm.TcmError):
+        sw.run_async()
+    sw.close()
+
+
 def test_engines_agree_on_heavy_load():
     tr, params = sweep(64, 1500, 41, kvs=(16384,), rates=(4.0,), mixes=((0.5, 0.2, 0.3),))
     _, a, sa = run_gpu(tr, params, tcm.ENGINE_FUSED)

@@ -29,6 +29,8 @@ torch.cuda.synchronize()
 T0 = time.perf_counter()
 ev = []
 loaded = threading.Event()
+gpu = threading.Lock()
+ASYNC = os.environ.get("E2E_ASYNC", "1") != "0"
 
 def worker(k):
     torch.cuda.set_device(dev)
@@ -39,9 +41,18 @@ def worker(k):
         a = time.perf_counter(); sim.load(host, res, mem=tcm.MEM_HOST); b = time.perf_counter()
         if k == 0 and i == 0:
             loaded.set()
-        sim.run(); c = time.perf_counter()
-        with torch.cuda.stream(st):
-            sim.aggregate(device=dev)
+        if ASYNC:
+            with gpu:
+                sim.run_async()
+                with torch.cuda.stream(st):
+                    sim.aggregate(device=dev)
+            c = time.perf_counter()
+            sim.wait(tcm.WAIT_ALL)
+        else:
+            sim.run()
+            c = time.perf_counter()
+            with torch.cuda.stream(st):
+                sim.aggregate(device=dev)
         d = time.perf_counter()
         ev.append((k, i, a - T0, b - T0, c - T0, d - T0))
 
