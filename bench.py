@@ -466,7 +466,21 @@ def run_tcm(args, rank, world, local):
 
     # end-to-end through the C ABI with HOST buffers (H2D + run + D2H inside the timed region)
     log("stepwise done")
+    e2e_skip = None
     if not args.skip_e2e:
+        # pinned host memory of the e2e leg on this node: the trace once and two contexts' results, per rank
+        per_rank = sum(trace[k].numel() * trace[k].element_size() for k in trace if k != "params") + 2 * 20 * N
+        local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        avail = host_mem_available()
+        bad = 1 if (avail is not None and local_ranks * per_rank > 0.85 * avail) else 0
+        if world > 1:                                  # every rank takes the same decision
+            flag = torch.tensor([bad], dtype=torch.int64, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            bad = int(flag[0])
+        if bad:
+            e2e_skip = (f"not run: {local_ranks} ranks x {per_rank / 1e9:.1f} GB of pinned host memory exceed 85 % of "
+                        f"this node's available {avail / 1e9:.0f} GB")
+    if not args.skip_e2e and e2e_skip is None:
         # free the device-resident run first: the two e2e contexts need ~74 GB each
         host = host_copy(trace)
         # a sample of the device-resident run's results: the e2e leg's outputs are checked against it
@@ -480,6 +494,8 @@ def run_tcm(args, rank, world, local):
         torch.cuda.empty_cache()
         out["e2e"] = bench_e2e(args, sw, host, dev, dist, world, (pick.cpu().numpy(), ref))
         del host
+    elif e2e_skip is not None:
+        out["e2e"] = {"value": None, "unit": "requests/s", "skipped": e2e_skip}
     log("e2e done")
 
     if not args.skip_next1 and args.workload == "c4" and rank == 0:
@@ -696,9 +712,25 @@ def bench_next1(args, dev, stream, engine=None, replicas=None, requests=None, po
 
 
 def host_copy(trace):
-    """Pinned host copies of the device trace (the e2e leg's inputs)."""
-    return {k: trace[k].cpu().pin_memory()
-            for k in ("req_offset", "arrival_us", "footprint", "inline_us", "out_tokens", "modality", "params")}
+    """Pinned host copies of the device trace (the e2e leg's inputs), copied straight into pinned memory."""
+    import torch
+    out = {}
+    for k in ("req_offset", "arrival_us", "footprint", "inline_us", "out_tokens", "modality", "params"):
+        x = trace[k]
+        out[k] = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        out[k].copy_(x)
+    return out
+
+
+def host_mem_available():
+    """MemAvailable of this node in bytes (Linux), or None."""
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
 
 
 def bench_e2e(args, sw, host, dev, dist, world, check):
