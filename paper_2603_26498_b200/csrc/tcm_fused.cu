@@ -738,8 +738,10 @@ void launch_fused(const ModelConst& m, const TraceDev& t, uint32_t max_iters, ui
 void launch_fused_stamp(const TraceDev& t, cudaStream_t s) {
     const uint32_t threads = 256;
     const uint64_t avg = t.R ? t.N / t.R : 0;
-    uint32_t wpr = 1;                                   // ~4k requests per warp, <= 4,096 warps in all
-    while (wpr < 64 && (uint64_t)wpr * 4096 < avg && (uint64_t)t.R * wpr * 2 <= 4096) wpr <<= 1;
+    // few huge replicas (C2: one queue of 100k) spread over up to 512 warps each, ~512 requests per warp;
+    // sweeps keep a warp per replica (<= 4,096 warps in all)
+    uint32_t wpr = 1;
+    while (wpr < 512 && (uint64_t)wpr * 512 < avg && (uint64_t)t.R * wpr * 2 <= 4096) wpr <<= 1;
     const uint64_t blocks = ((uint64_t)t.R * wpr * 32 + threads - 1) / threads;
     k_fstamp<<<(uint32_t)blocks, threads, 0, s>>>(t, wpr);
 }
