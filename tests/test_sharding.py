@@ -103,3 +103,15 @@ def test_c5_and_growth_sweeps_shard_cleanly():
         a, b = int(tr.offset[r]), int(tr.offset[r + 1])
         kv = int(sw.params["kv_capacity"][r])
         assert np.all(tr.footprint[a:b].astype(np.int64) + tr.out_tokens[a:b] - 1 <= kv)
+
+
+def test_c4_sweep_ids_cover_the_rank_ids():
+    """Sweep.ids (the global replica id of each loaded replica, after the C4 warp layout) is a permutation
+    of the rank's rank_ids, and the ranks of a world partition the single-rank sweep."""
+    full = W.c4(0, 1, replicas_per_gpu=1024, n_requests=10)
+    assert sorted(full.ids.tolist()) == sorted(W.rank_ids(len(full.cells), 1024 // len(full.cells), 0, 1))
+    parts = [W.c4(r, 2, replicas_per_gpu=512, n_requests=10).ids.tolist() for r in range(2)]
+    assert sorted(parts[0] + parts[1]) == sorted(full.ids.tolist())
+    # every replica's cell and generator record follow its global id
+    for j, g in enumerate(full.ids[:64]):
+        assert int(full.params["cell_id"][j]) == int(g) % len(full.cells)
